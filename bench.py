@@ -1,0 +1,520 @@
+#!/usr/bin/env python
+"""Benchmark of the tiled MonarchAttention forward (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config sf] [--impl ours|reference]
+
+A step is one tiled MonarchAttention forward over one synthetic layer of the
+configured workload (default C2: one Self-Forcing chunk, B=1 H=12 d=128,
+(f,h,w)=(3,30,52), (h,w)-tiled plan, T=1, bf16) on each rank (weak scaling:
+every GPU processes its own layer; layers are independent (b,h) problems, so
+there is no collective in the data path).  ``value`` is whole-job ms per
+layer = max-over-ranks device time per step / N.
+
+Timing: W warm-up steps, then K steps timed with CUDA events on the launching
+stream; a 256 MB buffer is rewritten between steps to flush L2 (126 MB), and
+the flush is outside the timed events.  Dense attention on the same shape
+(cuDNN SDPA, flash_attn, flashinfer) is timed identically; the fastest is the
+"dense FA" denominator.  ``--impl reference`` times the unmodified reference
+CPU implementation (baseline/_ref, falling back to the oracle port) on the
+host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MonarchAttn fwd ms/layer at Self-Forcing shape; speedup vs dense FA; TC util %"
+
+CONFIGS = {
+    # name: (B, H, f_kv, f_q, h, w, d, neighborhoods, dtype, description)
+    "sf": (1, 12, 3, 3, 30, 52, 128, (1, 30, 52), "bf16",
+           "C2 Self-Forcing chunk: B=1 H=12 d=128, 3 frames x 1560 tokens, (h,w)-tiled plan"),
+    "sf3hw": (1, 12, 3, 3, 30, 52, 128, (3, 30, 52), "bf16",
+              "C2' Self-Forcing chunk, (3h,w) plan = untiled (90,52)"),
+    "kv21": (1, 12, 21, 3, 30, 52, 128, (1, 30, 52), "bf16",
+             "C3 chunked-KV rollout: 3 query frames vs 21 KV frames, (h,w)-tiled"),
+    "n32k": (1, 12, 21, 21, 30, 52, 128, (1, 30, 52), "bf16",
+             "C4 N=32760 (21,30,52), (h,w)-tiled G=21"),
+    "c1": (1, 2, 1, 1, 32, 32, 64, None, "fp32",
+           "C1 CPU-reference config: B=1 H=2 N=1024 (32,32) untiled fp32"),
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            j = json.load(fh)
+        return {"hbm": j["hbm_gbs"], "tc_burst": j["bf16_tflops"],
+                "tc_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]), "src": "measured"}
+    except Exception:
+        return {"hbm": 6650.0, "tc_burst": 1590.0, "tc_sustained": 1400.0, "src": "fallback"}
+
+
+def workload(name, iterations):
+    import paper_2602_12271_b200 as pk
+
+    B, H, fkv, fq, h, w, d, nb, dt, desc = CONFIGS[name]
+    shape = pk.VideoShape(fkv, h, w)
+    if nb is None:
+        plan = pk.aligned_config(shape, ("f", "h"))
+        low = pk.lower_square(plan)
+    else:
+        plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
+        low = pk.lower_chunked(plan, fq) if fq != fkv else pk.lower_square(plan)
+    return dict(B=B, H=H, fkv=fkv, fq=fq, h=h, w=w, d=d, dv=d, nb=nb, dtype=dt, desc=desc,
+                plan=plan, low=low, T=iterations, nq=fq * h * w, nk=fkv * h * w)
+
+
+def algorithmic(wl):
+    """Per-layer useful FLOPs by stage and compulsory bytes."""
+    low, T, d, dv = wl["low"], wl["T"], wl["d"], wl["dv"]
+    gq, gk = low.c1_q * low.c2, low.c1_kv * low.c2
+    s1, s2 = low.s1, low.s2
+    units = wl["B"] * wl["H"]
+    eb = 2 if wl["dtype"] == "bf16" else 4
+    # row stage (∝ s1 s2^2): beta_R and alpha_L every iteration, Y once
+    row = units * gq * gk * s1 * s2 * s2 * 2 * (2 * T * d + dv)
+    # column stage: beta_L T times, O once, alpha_R (T-1) times  (∝ s2 s1^2)
+    col = units * gq * gk * s2 * s1 * s1 * 2 * (T * d + dv + (T - 1) * d)
+    total = row + col
+    bytes_ = units * (2 * wl["nq"] * d + wl["nk"] * (d + dv)) * eb
+    dense = units * 2 * wl["nq"] * wl["nk"] * (d + dv)
+    return dict(row=row, col=col, total=total, bytes=bytes_, dense=dense)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                self.lines = []
+
+    def summary(self):
+        sms, maxs, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sms:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(maxs), "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def time_steps(fn, steps, warmup, flush, stream):
+    """Sum of per-step CUDA-event times (ms) over `steps` steps, L2 flushed between."""
+    import torch
+
+    for _ in range(warmup):
+        flush()
+        fn()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in evs:
+        flush()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs)
+
+
+def dense_baselines(wl, q, k, v, steps, warmup, flush, stream):
+    import torch
+
+    res = {}
+    qh, kh, vh = (x.transpose(1, 2).contiguous() for x in (q, k, v))   # (B, N, H, d)
+
+    def sdpa_cudnn():
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            return torch.nn.functional.scaled_dot_product_attention(q, k, v)
+
+    def sdpa_flash():
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+
+        with sdpa_kernel([SDPBackend.FLASH_ATTENTION]):
+            return torch.nn.functional.scaled_dot_product_attention(q, k, v)
+
+    def fa2():
+        from flash_attn import flash_attn_func
+
+        return flash_attn_func(qh, kh, vh)
+
+    def flashinfer_prefill():
+        import flashinfer
+
+        return [flashinfer.single_prefill_with_kv_cache(qh[b], kh[b], vh[b]) for b in range(qh.shape[0])]
+
+    cands = [("torch_sdpa_cudnn", sdpa_cudnn), ("torch_sdpa_flash", sdpa_flash),
+             ("flash_attn_2.8", fa2), ("flashinfer_single_prefill", flashinfer_prefill)]
+    for name, fn in cands:
+        try:
+            fn()
+            torch.cuda.synchronize()
+            ms = time_steps(fn, steps, warmup, flush, stream) / steps
+            res[name] = round(ms, 5)
+        except Exception as e:   # backend unavailable for this shape/dtype
+            res[name] = f"unavailable: {type(e).__name__}: {str(e)[:80]}"
+    return res
+
+
+# --------------------------------------------------------------------------
+# reference CPU arm
+# --------------------------------------------------------------------------
+
+def _ref_worker(args):
+    """One (b,h) unit through the unmodified reference (or the oracle port)."""
+    import numpy as np
+
+    kind, cfg_name, T, seed = args
+    wl = workload(cfg_name, T)
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((wl["nq"], wl["d"])).astype(np.float32)
+    k = rng.standard_normal((wl["nk"], wl["d"])).astype(np.float32)
+    v = rng.standard_normal((wl["nk"], wl["dv"])).astype(np.float32)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        import monarchbench as mb
+
+        shape = mb.VideoShape(wl["fkv"], wl["h"], wl["w"])
+        if wl["nb"] is None:
+            cfg = mb.aligned_config(shape, ("f", "h"))
+            fac, _ = mb.solve(mb.AttentionProblem(q, k, v, shape), cfg, mb.SolverConfig(iterations=T))
+            mb.attention_output(fac, v)
+        else:
+            plan = mb.make_tile_plan(shape, mb.aligned_config(shape, ("f", "h")), wl["nb"])
+            qq = q
+            if wl["fq"] != wl["fkv"]:   # chunked-KV via the square embedding
+                qq = np.vstack([np.zeros((wl["nk"] - wl["nq"], wl["d"]), np.float32), q])
+            fac, _ = mb.solve_tiled(mb.AttentionProblem(qq, k, v, shape), plan, mb.SolverConfig(iterations=T))
+            mb.attention_output(fac, v)
+    else:
+        from oracle import monarch_oracle as orc
+
+        low = wl["low"]
+        oq = np.arange(low.n_q) if low.q_order is None else low.q_order
+        ok = np.arange(low.n_kv) if low.kv_order is None else low.kv_order
+        orc.forward_phi(q, k, v, oq, ok, low.c1_q, low.c1_kv, low.c2, low.s1, low.s2, T)
+    return time.perf_counter() - t0
+
+
+def _ref_kind():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "monarchbench")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        return "reference"
+    return "port"
+
+
+def cpu_layer_ms(cfg_name, T, units, cores, kind, max_units=None):
+    """Wall ms to run `units` (b,h) problems over a process pool of `cores`."""
+    import multiprocessing as mp
+
+    n = units if max_units is None else min(units, max_units)
+    jobs = [(kind, cfg_name, T, 1000 + i) for i in range(n)]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    if cores > 1:
+        with ctx.Pool(min(cores, n)) as pool:
+            pool.map(_ref_worker, jobs)
+    else:
+        for j in jobs:
+            _ref_worker(j)
+    wall = time.perf_counter() - t0
+    return wall * 1e3 * units / n, n
+
+
+def _env_threads():
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(var, "1")
+
+
+def run_reference(args):
+    _env_threads()
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = workload(args.config, args.iters)
+    kind = _ref_kind()
+    cores = len(os.sched_getaffinity(0))
+    units = wl["B"] * wl["H"]
+    for _ in range(args.warmup):
+        cpu_layer_ms(args.config, args.iters, units, cores, kind, max_units=min(units, cores))
+    times = [cpu_layer_ms(args.config, args.iters, units, cores, kind)[0] for _ in range(args.steps)]
+    ms = sum(times) / len(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/layer",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic N(0,1) q/k/v (seeded)",
+        "config": {"workload": wl["desc"], "iterations": args.iters, "units_per_step": units},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/layer", "cores": cores, "kind": kind,
+                         "sample": f"full layer ({units} (b,h) units) per step, process pool of {cores}, "
+                                   "numpy single-threaded per unit"},
+        "e2e": {"value": round(ms, 3), "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_12271_b200 as pk
+    from paper_2602_12271_b200 import _lib, ops
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    wl = workload(args.config, args.iters)
+    dtype = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    B, H = wl["B"], wl["H"]
+    q = torch.randn(B, H, wl["nq"], wl["d"], device=dev, dtype=dtype, generator=g)
+    k = torch.randn(B, H, wl["nk"], wl["d"], device=dev, dtype=dtype, generator=g)
+    v = torch.randn(B, H, wl["nk"], wl["dv"], device=dev, dtype=dtype, generator=g)
+    out = torch.empty(B, H, wl["nq"], wl["dv"], device=dev, dtype=dtype)
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        flush_buf.zero_()
+
+    low = wl["low"]
+    lib = _lib.load()
+    prep = ops.prepare(q, k, v, out, low, wl["T"])
+    nbytes = lib.mbx_workspace_bytes(prep.desc)
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    path = {0: "simt", 1: "tcgen05"}[lib.mbx_selected_path(prep.desc)]
+    import ctypes
+
+    def step():
+        st = lib.mbx_forward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                             out.data_ptr(), None, None, ws.data_ptr(), nbytes, stream.cuda_stream)
+        if st != 0:
+            _lib.check(st)
+
+    # ---- timed region (device time, max over ranks) ----
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        total_ms = time_steps(step, args.steps, args.warmup, flush, stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = ms_step / world                      # whole-job ms per layer
+
+    # ---- per-kernel shares (same stream, L2 flushed, CUDA events per launch) ----
+    prof_steps = max(3, min(args.steps, 50))
+    lib.mbx_profile_enable(1)
+    for _ in range(prof_steps):
+        flush()
+        step()
+    lib.mbx_profile_enable(0)
+    recs = _lib.profile_collect()
+    per = {}
+    for name, ms in recs:
+        per.setdefault(name, []).append(ms)
+    launches_per_step = len(recs) / prof_steps
+    kernels = [{"name": n, "ms_avg": round(sum(v_) / len(v_), 5), "launches_per_step": len(v_) / prof_steps}
+               for n, v_ in per.items()]
+    alg = algorithmic(wl)
+    peaks = _peaks()
+    ksum = sum(kk["ms_avg"] * kk["launches_per_step"] for kk in kernels) or ms_step
+    for kk in kernels:
+        kk["share"] = round(kk["ms_avg"] * kk["launches_per_step"] / ksum, 4)
+    dom = max(kernels, key=lambda kk: kk["ms_avg"] * kk["launches_per_step"]) if kernels else None
+    roofline = None
+    if dom is not None:
+        name = dom["name"]
+        per_launch = 1.0 / max(dom["launches_per_step"], 1e-9)
+        if "row" in name:
+            flops = alg["row"] * per_launch
+            byts = (wl["B"] * wl["H"]) * (wl["nq"] * wl["d"] + wl["nk"] * (wl["d"] + wl["dv"])) * (2 if dtype == torch.bfloat16 else 4)
+        elif "column" in name:
+            flops = alg["col"] * per_launch
+            byts = (wl["B"] * wl["H"]) * (wl["nq"] * (wl["d"] + wl["dv"])) * (2 if dtype == torch.bfloat16 else 4)
+        else:
+            flops, byts = alg["total"], alg["bytes"]
+        t_s = dom["ms_avg"] * 1e-3
+        t_tc = flops / (peaks["tc_burst"] * 1e12)
+        t_hbm = byts / (peaks["hbm"] * 1e9)
+        if t_tc >= t_hbm:
+            ach = flops / t_s / 1e12
+            roofline = {"bound": "tensor", "achieved": round(ach, 2), "peak": peaks["tc_burst"],
+                        "unit": "TFLOP/s", "frac": round(ach / peaks["tc_burst"], 4)}
+        else:
+            ach = byts / t_s / 1e9
+            roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"],
+                        "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4)}
+        roofline.update({"kernel": name, "traffic": _ncu_traffic(name, args.config),
+                         "peak_source": f"{peaks['src']} (MEASURED_PEAKS.json burst)",
+                         "algorithmic_flops_per_launch": int(flops), "algorithmic_bytes_per_launch": int(byts)})
+
+    # ---- end-to-end through the public API with host buffers ----
+    pin = [x.cpu().pin_memory() for x in (q, k, v)]
+    out_h = torch.empty(out.shape, dtype=dtype).pin_memory()
+    qd, kd, vd = (torch.empty_like(x) for x in (q, k, v))
+    plan = wl["plan"]
+    kvf = wl["fkv"] if wl["fq"] != wl["fkv"] else None
+
+    def e2e_step():
+        qd.copy_(pin[0], non_blocking=True)
+        kd.copy_(pin[1], non_blocking=True)
+        vd.copy_(pin[2], non_blocking=True)
+        o = pk.monarch_attention(qd, kd, vd, plan, iterations=wl["T"], kv_frames=kvf)
+        out_h.copy_(o, non_blocking=True)
+
+    e2e_total = time_steps(e2e_step, args.steps, args.warmup, flush, stream)
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_ms = e2e_total / args.steps / world
+    eb = 2 if dtype == torch.bfloat16 else 4
+    h2d = sum(x.numel() for x in pin) * eb
+    d2h = out_h.numel() * eb
+
+    # ---- dense attention on the same shape ----
+    dense = {}
+    if not args.no_dense and rank == 0:
+        dense = dense_baselines(wl, q, k, v, args.steps, args.warmup, flush, stream)
+    dense_nums = {kname: val for kname, val in dense.items() if isinstance(val, float)}
+    best_dense = min(dense_nums.values()) if dense_nums else None
+
+    # ---- CPU baseline (rank 0, N=1 only; bounded sample) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        _env_threads()
+        kind = _ref_kind()
+        cores = len(os.sched_getaffinity(0))
+        units = wl["B"] * wl["H"]
+        sample_units = min(units, max(cores, 2))
+        ms_cpu, n_done = cpu_layer_ms(args.config, wl["T"], units, cores, kind, max_units=sample_units)
+        cpu = {"value": round(ms_cpu, 2), "unit": "ms/layer", "cores": min(cores, n_done), "kind": kind,
+               "sample": f"{n_done} of {units} (b,h) units of one layer over a pool of "
+                         f"{min(cores, n_done)} processes, extrapolated linearly to {units} units"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 5), "unit": "ms/layer", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": wl["dtype"], "data": "synthetic N(0,1) q/k/v generated on device (seeded)",
+            "config": {"workload": wl["desc"], "B": B, "H": H, "frames_q": wl["fq"], "frames_kv": wl["fkv"],
+                       "h": wl["h"], "w": wl["w"], "d": wl["d"], "plan": plan.descriptor(),
+                       "iterations": wl["T"], "layers_per_rank_per_step": 1, "parallelism": f"dp{world} (b,h) shards",
+                       "l2": "flushed between timed steps (256 MB rewrite, outside events)", "path": path},
+            "dense_fa_ms": dense, "dense_fa_best_ms": best_dense,
+            "speedup_vs_dense": round(best_dense / ms_step, 3) if best_dense else None,
+            "effective_tflops": round(alg["total"] / (ms_step * 1e-3) / 1e12, 2),
+            "tc_util": round(alg["total"] / (ms_step * 1e-3) / 1e12 / peaks["tc_burst"], 4),
+            "algorithmic": {"flops_per_layer": alg["total"], "bytes_per_layer": alg["bytes"],
+                            "dense_flops_per_layer": alg["dense"]},
+            "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_ms, 5), "unit": "ms/layer", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel, config):
+    """dram bytes per launch of `kernel` from the committed ncu summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            j = json.load(fh)
+        return j.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="sf", choices=sorted(CONFIGS))
+    ap.add_argument("--iters", type=int, default=1)
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

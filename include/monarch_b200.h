@@ -1,0 +1,146 @@
+/*
+ * monarch_b200.h — C ABI of the B200-native tiled MonarchAttention forward.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/monarchbench):
+ *
+ *   mbx_forward   replaces  solve_tiled(problem, plan, solver)  solver.py:161-204
+ *                           + attention_output(factors, v)      solver.py:207-217
+ *                           and, with c1 = c2 = 1, solve(...)   solver.py:114-158
+ *                           (factors optional: L', R' in the TiledMonarchFactors
+ *                           layout, factors.py:57-79)
+ *   mbx_apply     replaces  apply_factors(factors, v)           factors.py:110-125
+ *                           via attention_output                solver.py:207-217
+ *
+ * All pointers are DEVICE pointers owned by the caller (the library never
+ * allocates or frees user memory).  All work is enqueued on `stream`
+ * (a cudaStream_t passed as void*); no call synchronizes the device.
+ * The descriptor is read during the call and not retained.
+ *
+ * Errors: every entry point returns an mbx_status; a non-zero status leaves a
+ * thread-local message readable with mbx_last_error().  The Python layer maps
+ * MBX_ERR_BAD_SHAPE / BAD_PLAN / BAD_ITERS / BAD_EPS to the reference's
+ * SolverError / LayoutError (ValueError subclasses, solver.py:25-26,
+ * layout.py:21-22).
+ */
+#ifndef MONARCH_B200_H
+#define MONARCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MBX_ABI_VERSION 1
+
+typedef enum mbx_status {
+    MBX_OK = 0,
+    MBX_ERR_BAD_SHAPE = 1,   /* inconsistent sizes / strides (SolverError, ShapeError)   */
+    MBX_ERR_BAD_PLAN = 2,    /* tiling does not divide the blocks (LayoutError)          */
+    MBX_ERR_BAD_ITERS = 3,   /* iterations < 1 (SolverConfig, solver.py:73-74)           */
+    MBX_ERR_BAD_EPS = 4,     /* eps outside (0, 1e-6] (solver.py:75-77)                  */
+    MBX_ERR_BAD_DTYPE = 5,
+    MBX_ERR_NULL = 6,        /* required pointer is NULL                                 */
+    MBX_ERR_WORKSPACE = 7,   /* workspace smaller than mbx_workspace_bytes()             */
+    MBX_ERR_UNSUPPORTED = 8, /* shape outside what the kernels implement (e.g. d > 256)  */
+    MBX_ERR_CUDA = 9         /* a CUDA launch failed                                     */
+} mbx_status;
+
+typedef enum mbx_dtype {
+    MBX_F32 = 0,   /* fp32 I/O, fp32 arithmetic (parity mode, 1e-4 rel-L2)   */
+    MBX_BF16 = 1   /* bf16 I/O, fp32 accumulate / softmax (2e-2 rel-L2)       */
+} mbx_dtype;
+
+/* flags */
+#define MBX_FLAG_FORCE_GENERIC 0x1  /* route to the SIMT kernels even if a tensor-core path applies */
+#define MBX_FLAG_NO_OUTPUT 0x2      /* factors only (solve_tiled without attention_output)          */
+
+/*
+ * One forward problem, batched over (batch, heads).  Tokens of a (b, h)
+ * slice live at  base + b*stride[0] + h*stride[1] + row*stride[2] (+ feature,
+ * contiguous).  Slot order: ordered index p of query tile-row l1, row l2,
+ * tile-column j1, column j2 is p = ((l1*s1 + l2)*c2 + j1)*s2 + j2 (the
+ * reshape of solver.py:178-179); q_order[p] / kv_order[p] give the token row
+ * it reads (TokenOrdering.to_phi, layout.py:89-94); NULL = identity.
+ *
+ * Square problems have c1_q == c1_kv.  Chunked-KV (causal autoregressive
+ * rollout) problems have c1_q < c1_kv: the queries are the last query-tile
+ * rows of the key grid, every query tile attends to every key tile.
+ */
+typedef struct mbx_desc {
+    int32_t abi_version;          /* must be MBX_ABI_VERSION */
+    int32_t dtype;                /* mbx_dtype for q, k, v and out */
+    int32_t batch, heads;
+    int32_t head_dim;             /* d   (q, k) */
+    int32_t v_dim;                /* d_v (v, out) */
+    int32_t c1_q, c1_kv, c2;      /* tile grid */
+    int32_t s1, s2;               /* tile shape (rows, columns) */
+    int32_t iterations;           /* T >= 1 (SolverConfig.iterations) */
+    int32_t flags;
+    float scale;                  /* logit scale applied to q (solver.py:58-60, 104) */
+    double eps_div;               /* SolverConfig.eps_div (solver.py:67, 188), in (0, 1e-6] */
+    double eps_log;               /* SolverConfig.eps_log (solver.py:68, 191), in (0, 1e-6];
+                                     c_L is evaluated as sum R z - lse, which equals
+                                     sum R log max(R, eps_log) up to terms < eps_log*|log eps_log| */
+    int64_t q_stride[3];          /* (batch, head, token) strides in elements */
+    int64_t k_stride[3];
+    int64_t v_stride[3];
+    int64_t o_stride[3];
+    const int32_t* q_order;       /* device, c1_q*s1*c2*s2 entries or NULL */
+    const int32_t* kv_order;      /* device, c1_kv*s1*c2*s2 entries or NULL */
+} mbx_desc;
+
+/* Library / ABI version (== MBX_ABI_VERSION for a matching build). */
+int mbx_version(void);
+
+/* Thread-local message for the last non-OK status on this thread. */
+const char* mbx_last_error(void);
+
+/* Validate a descriptor without launching anything. */
+int mbx_validate(const mbx_desc* desc);
+
+/* Device workspace the forward needs (bytes, 256-byte aligned). */
+size_t mbx_workspace_bytes(const mbx_desc* desc);
+
+/* 0 = SIMT generic kernels, 1 = tcgen05 tensor-core kernels. */
+int mbx_selected_path(const mbx_desc* desc);
+
+/*
+ * Forward: T alternating R/L refinements followed by O = L (R V).
+ * out (optional if MBX_FLAG_NO_OUTPUT) is written in token (phi) order.
+ * l_factor / r_factor (optional, fp32, per (b,h) contiguous) receive the final
+ * L' (c1_q,c2,c1_kv,c2,s2,s1,s1) and R' (c1_q,c2,c1_kv,c2,s1,s2,s2).
+ */
+int mbx_forward(const mbx_desc* desc, const void* q, const void* k, const void* v,
+                void* out, float* l_factor, float* r_factor,
+                void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Block-apply of given factors (apply_factors, factors.py:110-125):
+ * out = L' (R' V) with V gathered through kv_order and out scattered through
+ * q_order.  Only v_dim, dtype, grid/tile sizes, v/o strides and orders are read.
+ */
+int mbx_apply(const mbx_desc* desc, const float* l_factor, const float* r_factor,
+              const void* v, void* out, void* workspace, size_t workspace_bytes,
+              void* stream);
+
+/* Workspace for mbx_apply (the Y = R V intermediate). */
+size_t mbx_apply_workspace_bytes(const mbx_desc* desc);
+
+/*
+ * Per-kernel timing for benchmarks (thread-local).  While enabled, every
+ * kernel the library launches is bracketed by CUDA events on its stream.
+ * mbx_profile_collect synchronizes those events, writes up to `max_entries`
+ * (name, milliseconds) pairs in launch order, clears the record and returns
+ * the number of launches recorded.
+ */
+int mbx_profile_enable(int on);
+int mbx_profile_collect(float* ms, const char** names, int max_entries);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MONARCH_B200_H */

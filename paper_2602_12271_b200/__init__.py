@@ -1,0 +1,54 @@
+"""B200-native tiled MonarchAttention (MonarchRT, arXiv 2602.12271).
+
+Drop-in for the hot path of the reference package ``monarchbench``:
+``solve`` / ``solve_tiled`` / ``attention_output`` with the same layout types,
+plus the batched CUDA operator ``monarch_attention`` over (B, H, N, d)
+tensors.  All arithmetic runs in the in-tree sm_100a library
+``libmonarch_b200.so`` through its C ABI (include/monarch_b200.h).
+"""
+
+from .layout import (
+    AXES,
+    AxisDigit,
+    BlockConfig,
+    LayoutError,
+    LayoutPermutation,
+    Lowered,
+    TilePlan,
+    TokenOrdering,
+    VideoShape,
+    aligned_config,
+    build_permutation,
+    config_from_sizes,
+    enumerate_aligned_configs,
+    flatten_index,
+    generalized_ordering,
+    lower_chunked,
+    lower_square,
+    make_tile_plan,
+    phi_ordering,
+    rho_ordering,
+)
+
+__all__ = [
+    "AXES", "AxisDigit", "BlockConfig", "LayoutError", "LayoutPermutation", "Lowered", "TilePlan",
+    "TokenOrdering", "VideoShape", "aligned_config", "build_permutation", "config_from_sizes",
+    "enumerate_aligned_configs", "flatten_index", "generalized_ordering", "lower_chunked",
+    "lower_square", "make_tile_plan", "phi_ordering", "rho_ordering",
+    "AttentionProblem", "SolverConfig", "SolverError", "SolverTrace", "MonarchFactors",
+    "TiledMonarchFactors", "FactorError", "ShapeError", "solve", "solve_tiled",
+    "attention_output", "monarch_attention",
+]
+
+
+def __getattr__(name):
+    # torch-dependent API is imported lazily so the layout mirror stays importable alone
+    if name in ("AttentionProblem", "SolverConfig", "SolverTrace", "MonarchFactors",
+                "TiledMonarchFactors", "FactorError", "ShapeError", "solve", "solve_tiled",
+                "attention_output"):
+        from . import solver
+        return getattr(solver, name)
+    if name in ("SolverError", "monarch_attention"):
+        from . import ops
+        return getattr(ops, name)
+    raise AttributeError(name)

@@ -1,0 +1,213 @@
+"""Batched torch-level operator over the C ABI.
+
+``monarch_attention(q, k, v, plan, ...)`` is the fast entry point: q, k, v are
+CUDA tensors (B, H, N, d) in token (phi) order, bf16 or fp32; the output has
+q's layout.  It lowers the plan (layout.Lowered), builds an ``mbx_desc`` and
+enqueues ``mbx_forward`` on torch's current stream.  No CPU fallback exists:
+CPU tensors or a missing library raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import functools
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .layout import LayoutError, Lowered, TilePlan, BlockConfig, lower_chunked, lower_square
+
+
+class SolverError(ValueError):
+    """Invalid problem or solver configuration (solver.py:25-26)."""
+
+
+_DTYPES = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}
+
+_order_cache: dict[tuple, tuple[np.ndarray, torch.Tensor]] = {}
+
+
+def _device_order(order: np.ndarray | None, device: torch.device) -> torch.Tensor | None:
+    """Upload a slot permutation once per (array, device); lowered plans are
+    cached, so their order arrays are long-lived."""
+    if order is None:
+        return None
+    key = (id(order), str(device))
+    hit = _order_cache.get(key)
+    if hit is None or hit[0] is not order:
+        hit = (order, torch.from_numpy(np.ascontiguousarray(order, dtype=np.int32)).to(device))
+        _order_cache[key] = hit
+    return hit[1]
+
+
+@functools.lru_cache(maxsize=256)
+def _lower_square_cached(plan):
+    return lower_square(plan)
+
+
+@functools.lru_cache(maxsize=256)
+def _lower_chunked_cached(plan, q_frames):
+    return lower_chunked(plan, q_frames)
+
+
+@dataclass
+class PreparedProblem:
+    """A descriptor plus the device buffers it points into (kept alive)."""
+
+    desc: _lib.MbxDesc
+    q_order: torch.Tensor | None
+    kv_order: torch.Tensor | None
+    workspace: torch.Tensor | None = None
+
+
+def _strides(t: torch.Tensor) -> tuple[int, int, int]:
+    if t.stride(-1) != 1:
+        raise SolverError("the feature dimension must be contiguous")
+    return (t.stride(0), t.stride(1), t.stride(2))
+
+
+def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor,
+            low: Lowered, iterations: int = 1, scale: float | None = None,
+            eps_div: float = 1e-30, eps_log: float = 1e-300, flags: int = 0) -> PreparedProblem:
+    if not (q.is_cuda and k.is_cuda and v.is_cuda and out.is_cuda):
+        raise SolverError("monarch_attention runs on CUDA tensors only (no CPU fallback)")
+    if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+        raise SolverError("q, k, v must be (B, H, N, d)")
+    if q.dtype not in _DTYPES or k.dtype != q.dtype or v.dtype != q.dtype or out.dtype != q.dtype:
+        raise SolverError(f"q, k, v, out must share dtype float32 or bfloat16, got {q.dtype}")
+    B, H, nq, d = q.shape
+    if k.shape[:2] != (B, H) or v.shape[:2] != (B, H):
+        raise SolverError("q, k, v batch/head dims differ")
+    if nq != low.n_q or k.shape[2] != low.n_kv or v.shape[2] != low.n_kv:
+        raise SolverError(f"token counts (q {nq}, k {k.shape[2]}, v {v.shape[2]}) do not match the "
+                          f"plan (q {low.n_q}, kv {low.n_kv})")
+    if k.shape[3] != d:
+        raise SolverError("q and k must share the head dimension")
+    if out.shape != (B, H, nq, v.shape[3]):
+        raise SolverError("out must be (B, H, N_q, d_v)")
+    if iterations < 1:
+        raise SolverError("iterations must be >= 1")
+    desc = _lib.MbxDesc()
+    desc.abi_version = _lib.ABI_VERSION
+    desc.dtype = _DTYPES[q.dtype]
+    desc.batch, desc.heads, desc.head_dim, desc.v_dim = B, H, d, v.shape[3]
+    desc.c1_q, desc.c1_kv, desc.c2, desc.s1, desc.s2 = low.c1_q, low.c1_kv, low.c2, low.s1, low.s2
+    desc.iterations = iterations
+    desc.flags = flags
+    desc.scale = float(scale) if scale is not None else 1.0 / math.sqrt(d)
+    desc.eps_div, desc.eps_log = eps_div, eps_log
+    for name, t in (("q_stride", q), ("k_stride", k), ("v_stride", v), ("o_stride", out)):
+        getattr(desc, name)[:] = _strides(t)
+    qo = _device_order(low.q_order, q.device)
+    ko = _device_order(low.kv_order, q.device)
+    desc.q_order = qo.data_ptr() if qo is not None else None
+    desc.kv_order = ko.data_ptr() if ko is not None else None
+    return PreparedProblem(desc, qo, ko)
+
+
+def _raise_mapped(err: _lib.MbxError):
+    if err.status == _lib.BAD_PLAN:
+        raise LayoutError(str(err)) from None
+    if err.status in (_lib.BAD_SHAPE, _lib.BAD_ITERS, _lib.BAD_EPS, _lib.BAD_DTYPE, _lib.UNSUPPORTED):
+        raise SolverError(str(err)) from None
+    raise err
+
+
+def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_log=1e-300,
+            out=None, return_factors=False, force_generic=False, workspace=None):
+    """Run ``mbx_forward``; returns out or (out, L', R') with fp32 factors of
+    shape (B, H, c1_q, c2, c1_kv, c2, s2, s1, s1) / (..., s1, s2, s2)."""
+    lib = _lib.load()
+    if out is None:
+        out = torch.empty(q.shape[:3] + (v.shape[3],), dtype=q.dtype, device=q.device)
+    flags = _lib.FLAG_FORCE_GENERIC if force_generic else 0
+    prep = prepare(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags)
+    lf = rf = None
+    if return_factors:
+        B, H = q.shape[:2]
+        lf = torch.empty((B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s2, low.s1, low.s1),
+                         dtype=torch.float32, device=q.device)
+        rf = torch.empty((B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s1, low.s2, low.s2),
+                         dtype=torch.float32, device=q.device)
+    try:
+        _lib.check(lib.mbx_validate(ctypes.byref(prep.desc)))
+    except _lib.MbxError as e:
+        _raise_mapped(e)
+    nbytes = lib.mbx_workspace_bytes(ctypes.byref(prep.desc))
+    if return_factors:   # factor export runs on the SIMT path; size its workspace
+        prep.desc.flags |= _lib.FLAG_FORCE_GENERIC
+        nbytes = lib.mbx_workspace_bytes(ctypes.byref(prep.desc))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device)
+    stream = torch.cuda.current_stream(q.device).cuda_stream
+    st = lib.mbx_forward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                         out.data_ptr(), lf.data_ptr() if lf is not None else None,
+                         rf.data_ptr() if rf is not None else None,
+                         workspace.data_ptr(), nbytes, stream)
+    try:
+        _lib.check(st)
+    except _lib.MbxError as e:
+        _raise_mapped(e)
+    if return_factors:
+        return out, lf, rf
+    return out
+
+
+def apply(l_factor: torch.Tensor, r_factor: torch.Tensor, v: torch.Tensor, low: Lowered,
+          out_dtype=None) -> torch.Tensor:
+    """``mbx_apply``: O = L' (R' V) for given fp32 factors (factors.py:110-125)."""
+    lib = _lib.load()
+    B, H = v.shape[:2]
+    q_like = torch.empty((B, H, low.n_q, v.shape[3]), dtype=v.dtype, device=v.device)
+    out = torch.empty_like(q_like)
+    prep = prepare(q_like, v, v, out, low)
+    nbytes = lib.mbx_apply_workspace_bytes(ctypes.byref(prep.desc))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=v.device)
+    st = lib.mbx_apply(ctypes.byref(prep.desc), l_factor.contiguous().data_ptr(),
+                       r_factor.contiguous().data_ptr(), v.data_ptr(), out.data_ptr(),
+                       ws.data_ptr(), nbytes, torch.cuda.current_stream(v.device).cuda_stream)
+    try:
+        _lib.check(st)
+    except _lib.MbxError as e:
+        _raise_mapped(e)
+    return out
+
+
+def selected_path(q, k, v, low: Lowered, iterations=1) -> str:
+    lib = _lib.load()
+    out = torch.empty(q.shape[:3] + (v.shape[3],), dtype=q.dtype, device=q.device)
+    prep = prepare(q, k, v, out, low, iterations)
+    return {0: "simt", 1: "tcgen05"}.get(lib.mbx_selected_path(ctypes.byref(prep.desc)), "invalid")
+
+
+def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = None,
+                      kv_frames: int | None = None, return_factors: bool = False,
+                      force_generic: bool = False):
+    """Tiled MonarchAttention forward on (B, H, N, d) CUDA tensors.
+
+    ``plan`` is a TilePlan (tiled, solver.py:161) or BlockConfig (untiled,
+    solver.py:114).  With ``kv_frames`` unset the problem is square; for a
+    chunked-KV rollout pass the plan over the full (f_kv, h, w) key grid and
+    q holding the last ``q_frames = q.shape[2] // (h*w)`` frames.
+    """
+    if kv_frames is None and q.shape[2] == k.shape[2]:
+        low = _lower_square_cached(plan)
+    else:
+        if not isinstance(plan, TilePlan):
+            raise LayoutError("chunked-KV needs a TilePlan")
+        s = plan.shape
+        if kv_frames is not None and kv_frames != s.f:
+            raise LayoutError(f"kv_frames {kv_frames} != plan frames {s.f}")
+        hw = s.h * s.w
+        if q.shape[2] % hw:
+            raise SolverError("query tokens are not a whole number of frames")
+        low = _lower_chunked_cached(plan, q.shape[2] // hw)
+    return forward(q, k, v, low, iterations, scale, return_factors=return_factors,
+                   force_generic=force_generic)
+
+
+__all__ = ["monarch_attention", "forward", "apply", "prepare", "selected_path", "SolverError",
+           "BlockConfig", "TilePlan"]

@@ -1,0 +1,178 @@
+"""GPU parity of the CUDA path against the reference goldens and the oracle.
+
+Tolerances (BASELINE.json north_star): fp32 kernels within 1e-4 relative L2,
+bf16 kernels within 2e-2 relative L2 of the fp64/fp32 reference output and
+factors.  Every call goes through the C ABI (libmonarch_b200.so).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2602_12271_b200 as pk
+from paper_2602_12271_b200 import ops
+from cases import case_inputs, oracle_lowering, package_lowering, package_plan
+from oracle import monarch_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4
+BF16_TOL = 2e-2
+
+
+def _t(x, dev, dtype=torch.float32):
+    return torch.as_tensor(np.asarray(x), dtype=dtype, device=dev)
+
+
+def test_library_is_the_cuda_path(cuda):
+    from paper_2602_12271_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.mbx_version() == _lib.ABI_VERSION
+
+
+def test_goldens_fp32_through_abi(goldens, cuda):
+    manifest, data = goldens
+    for meta in manifest:
+        q, k, v = case_inputs(meta, data)
+        low = package_lowering(meta)
+        out, lf, rf = ops.forward(_t(q, cuda)[None, None], _t(k, cuda)[None, None],
+                                  _t(v, cuda)[None, None], low, meta["T"], return_factors=True)
+        name = meta["name"]
+        ref = data[f"{name}/out"]
+        assert orc.rel_l2(out[0, 0].cpu().numpy(), ref) < FP32_TOL, name
+        if f"{name}/L" in data:
+            assert orc.rel_l2(lf[0, 0].cpu().numpy(), data[f"{name}/L"]) < FP32_TOL, name
+            assert orc.rel_l2(rf[0, 0].cpu().numpy(), data[f"{name}/R"]) < FP32_TOL, name
+
+
+def test_reference_api_drop_in(goldens, cuda):
+    """solve / solve_tiled + attention_output with the reference's call shapes."""
+    manifest, data = goldens
+    for meta in manifest:
+        if meta["kind"] == "chunk":
+            continue
+        q, k, v = case_inputs(meta, data)
+        shape = pk.VideoShape(*meta["shape"])
+        plan = package_plan(meta)
+        problem = pk.AttentionProblem(q, k, v, shape)
+        cfg = pk.SolverConfig(iterations=meta["T"])
+        if meta["kind"] == "solve":
+            fac, trace = pk.solve(problem, plan, cfg)
+            assert isinstance(fac, pk.MonarchFactors)
+        else:
+            fac, trace = pk.solve_tiled(problem, plan, cfg)
+            assert isinstance(fac, pk.TiledMonarchFactors)
+        assert trace.objectives == [] and fac.order is not None
+        out = pk.attention_output(fac, v)
+        assert out.dtype == np.float64 and out.shape == (shape.n, v.shape[1])
+        name = meta["name"]
+        assert orc.rel_l2(out, data[f"{name}/out"]) < FP32_TOL, name
+        if f"{name}/L" in data:
+            L = data[f"{name}/L"]
+            R = data[f"{name}/R"]
+            if meta["kind"] == "solve":
+                L, R = L[0, 0, 0, 0], R[0, 0, 0, 0]
+            assert orc.rel_l2(fac.l_blocks, L) < FP32_TOL, name
+            assert orc.rel_l2(fac.r_blocks, R) < FP32_TOL, name
+
+
+def test_solver_errors_match_reference(cuda):
+    s = pk.VideoShape(2, 3, 3)
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((18, 4))
+    with pytest.raises(pk.SolverError):
+        pk.SolverConfig(iterations=0)
+    with pytest.raises(pk.SolverError):
+        bad = q.copy()
+        bad[0, 0] = np.nan
+        pk.AttentionProblem(bad, q, q, s)
+    problem = pk.AttentionProblem(q, q, q, s)
+    with pytest.raises(pk.SolverError):
+        pk.solve(problem, pk.aligned_config(pk.VideoShape(1, 3, 6), ("f", "h")))
+    with pytest.raises(pk.SolverError):
+        pk.solve(problem, pk.aligned_config(s, ("f", "h")), pk.SolverConfig(trace_mse=True))
+    with pytest.raises(pk.ShapeError):
+        fac, _ = pk.solve(problem, pk.aligned_config(s, ("f", "h")))
+        pk.attention_output(fac, q[:5])
+
+
+def _sf_plan(f=3, h=30, w=52, nb=None):
+    s = pk.VideoShape(f, h, w)
+    return pk.make_tile_plan(s, pk.aligned_config(s, ("f", "h")), nb or (1, h, w))
+
+
+def _oracle_heads(q, k, v, low, T, scale=None):
+    """fp64 oracle per (b, h) of (B, H, N, d) tensors."""
+    qn, kn, vn = (x.float().cpu().numpy().astype(np.float64) for x in (q, k, v))
+    oq = np.arange(low.n_q) if low.q_order is None else low.q_order
+    ok = np.arange(low.n_kv) if low.kv_order is None else low.kv_order
+    out = np.empty(q.shape[:3] + (v.shape[3],))
+    for b in range(q.shape[0]):
+        for h in range(q.shape[1]):
+            _, _, out[b, h] = orc.forward_phi(qn[b, h], kn[b, h], vn[b, h], oq, ok, low.c1_q,
+                                              low.c1_kv, low.c2, low.s1, low.s2, T, scale)
+    return out
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, FP32_TOL), (torch.bfloat16, BF16_TOL)])
+@pytest.mark.parametrize("T", [1, 2, 3])
+def test_self_forcing_chunk_shape(cuda, dtype, tol, T):
+    """C2 shape (3 frames x 30x52, d=128, (h,w) tiles) on 2 heads vs the oracle."""
+    g = torch.Generator(device="cpu").manual_seed(T)
+    q, k, v = (torch.randn(1, 2, 4680, 128, generator=g).to(cuda, dtype) for _ in range(3))
+    plan = _sf_plan()
+    out = pk.monarch_attention(q, k, v, plan, iterations=T)
+    ref = _oracle_heads(q, k, v, pk.lower_square(plan), T)
+    assert orc.rel_l2(out.float().cpu().numpy(), ref) < tol
+
+
+@pytest.mark.parametrize("T", [1, 2])
+def test_chunked_kv_rollout(cuda, T):
+    """3 query frames vs 7 KV frames, (h,w) tiles — rectangular tile grid."""
+    g = torch.Generator(device="cpu").manual_seed(11)
+    fkv, fq, h, w = 7, 3, 30, 52
+    q = torch.randn(1, 1, fq * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k = torch.randn(1, 1, fkv * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    v = torch.randn(1, 1, fkv * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    plan = _sf_plan(fkv, h, w)
+    out = pk.monarch_attention(q, k, v, plan, iterations=T, kv_frames=fkv)
+    ref = _oracle_heads(q, k, v, pk.lower_chunked(plan, fq), T)
+    assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
+
+
+def test_strided_batch_heads_and_permuted_plan(cuda):
+    """(B, N, H, d) storage viewed as (B, H, N, d); neighborhood plan with c2 > 1."""
+    g = torch.Generator(device="cpu").manual_seed(3)
+    B, H, f, h, w, d = 2, 3, 4, 6, 8, 32
+    n = f * h * w
+    base = [torch.randn(B, n, H, d, generator=g).to(cuda) for _ in range(3)]
+    q, k, v = (x.permute(0, 2, 1, 3) for x in base)
+    plan = _sf_plan(f, h, w, (2, 3, 4))
+    out = pk.monarch_attention(q, k, v, plan, iterations=2)
+    ref = _oracle_heads(q, k, v, pk.lower_square(plan), 2)
+    assert orc.rel_l2(out.cpu().numpy(), ref) < FP32_TOL
+
+
+def test_deterministic_bitwise(cuda):
+    g = torch.Generator(device="cpu").manual_seed(4)
+    q, k, v = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    plan = _sf_plan()
+    a = pk.monarch_attention(q, k, v, plan)
+    b = pk.monarch_attention(q, k, v, plan)
+    assert torch.equal(a, b)
+
+
+def test_factors_row_stochastic_on_device(cuda):
+    g = torch.Generator(device="cpu").manual_seed(5)
+    q, k, v = (torch.randn(1, 1, 4 * 6 * 8, 16, generator=g).to(cuda) for _ in range(3))
+    plan = _sf_plan(4, 6, 8, (2, 3, 4))
+    _, lf, rf = pk.monarch_attention(q, k, v, plan, iterations=3, return_factors=True)
+    assert (rf.sum(-1) - 1).abs().max().item() < 1e-5
+    assert (lf.sum(dim=(4, 5, 8)) - 1).abs().max().item() < 1e-5
+
+
+def test_rejects_cpu_tensors():
+    q = torch.zeros(1, 1, 4680, 128)
+    with pytest.raises(pk.SolverError):
+        pk.monarch_attention(q, q, q, _sf_plan())
