@@ -90,6 +90,14 @@ typedef struct mbx_desc {
     int64_t o_stride[3];
     const int32_t* q_order;       /* device, c1_q*s1*c2*s2 entries or NULL */
     const int32_t* kv_order;      /* device, c1_kv*s1*c2*s2 entries or NULL */
+    /* Optional closed form of the orders for neighborhood tile plans
+     * (make_tile_plan, layout.py:319-351): key grid (f_kv, h, w) and
+     * neighborhood (n_f, n_h, n_w).  nbhd[0] == 0 means "orders only".  When
+     * set, it must describe the same permutation as q_order / kv_order; the
+     * tensor-core path addresses tile rows with it (permutation folded into
+     * TMA coordinates, no gather). */
+    int32_t grid[3];
+    int32_t nbhd[3];
 } mbx_desc;
 
 /* Library / ABI version (== MBX_ABI_VERSION for a matching build). */
@@ -106,6 +114,12 @@ size_t mbx_workspace_bytes(const mbx_desc* desc);
 
 /* 0 = SIMT generic kernels, 1 = tcgen05 tensor-core kernels. */
 int mbx_selected_path(const mbx_desc* desc);
+
+/* Host-side: token row that slot `slot` of the query (is_query=1) or key grid
+ * reads under the descriptor's closed-form addressing (identity when no
+ * neighborhood is given).  -1 on invalid input.  Lets callers check the
+ * closed form against their order arrays without a GPU. */
+int64_t mbx_token_index(const mbx_desc* desc, int is_query, int64_t slot);
 
 /*
  * Forward: T alternating R/L refinements followed by O = L (R V).

@@ -22,7 +22,7 @@ OK, BAD_SHAPE, BAD_PLAN, BAD_ITERS, BAD_EPS, BAD_DTYPE, NULL, WORKSPACE, UNSUPPO
 
 EXPORTS = ("mbx_version", "mbx_last_error", "mbx_validate", "mbx_workspace_bytes",
            "mbx_selected_path", "mbx_forward", "mbx_apply", "mbx_apply_workspace_bytes",
-           "mbx_profile_enable", "mbx_profile_collect")
+           "mbx_profile_enable", "mbx_profile_collect", "mbx_token_index")
 
 
 class MbxDesc(ctypes.Structure):
@@ -49,6 +49,8 @@ class MbxDesc(ctypes.Structure):
         ("o_stride", ctypes.c_int64 * 3),
         ("q_order", ctypes.c_void_p),
         ("kv_order", ctypes.c_void_p),
+        ("grid", ctypes.c_int32 * 3),
+        ("nbhd", ctypes.c_int32 * 3),
     ]
 
 
@@ -86,6 +88,8 @@ def load() -> ctypes.CDLL:
     lib.mbx_forward.restype = ctypes.c_int
     lib.mbx_apply.argtypes = [ctypes.POINTER(MbxDesc), vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.mbx_apply.restype = ctypes.c_int
+    lib.mbx_token_index.argtypes = [ctypes.POINTER(MbxDesc), ctypes.c_int, ctypes.c_int64]
+    lib.mbx_token_index.restype = ctypes.c_int64
     lib.mbx_profile_enable.argtypes = [ctypes.c_int]
     lib.mbx_profile_enable.restype = ctypes.c_int
     lib.mbx_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_char_p),

@@ -55,6 +55,16 @@ int validate(const mbx_desc* d, mbx::Geometry* g) {
     for (int i = 0; i < 3; ++i)
         if (d->q_stride[i] < 0 || d->k_stride[i] < 0 || d->v_stride[i] < 0 || d->o_stride[i] < 0)
             return fail(MBX_ERR_BAD_SHAPE, "negative stride");
+    if (d->nbhd[0] > 0) {
+        const int F = d->grid[0], H = d->grid[1], W = d->grid[2];
+        const int nf = d->nbhd[0], nh = d->nbhd[1], nw = d->nbhd[2];
+        if (F < 1 || H < 1 || W < 1 || nh < 1 || nw < 1 || F % nf || H % nh || W % nw)
+            return fail(MBX_ERR_BAD_PLAN, "neighborhood (%d,%d,%d) must divide grid (%d,%d,%d)", nf, nh, nw,
+                        F, H, W);
+        if (d->s1 != nf * nh || d->s2 != nw || d->c2 != W / nw || d->c1_kv != (F / nf) * (H / nh) ||
+            d->c1_q % (H / nh))
+            return fail(MBX_ERR_BAD_PLAN, "neighborhood description inconsistent with the tile grid");
+    }
     if (d->q_stride[2] < d->head_dim || d->k_stride[2] < d->head_dim || d->v_stride[2] < d->v_dim ||
         d->o_stride[2] < d->v_dim)
         return fail(MBX_ERR_BAD_SHAPE, "token stride smaller than the feature width");
@@ -83,6 +93,12 @@ int validate(const mbx_desc* d, mbx::Geometry* g) {
         }
         g->q_order = d->q_order;
         g->kv_order = d->kv_order;
+        g->F = d->grid[0];
+        g->H = d->grid[1];
+        g->W = d->grid[2];
+        g->nf = d->nbhd[0] > 0 ? d->nbhd[0] : 0;
+        g->nh = d->nbhd[1];
+        g->nw = d->nbhd[2];
     }
     return MBX_OK;
 }
@@ -166,6 +182,18 @@ int mbx_profile_collect(float* ms, const char** names, int max_entries) {
 const char* mbx_last_error(void) { return g_last_error.c_str(); }
 
 int mbx_validate(const mbx_desc* desc) { return validate(desc, nullptr); }
+
+int64_t mbx_token_index(const mbx_desc* desc, int is_query, int64_t slot) {
+    mbx::Geometry g;
+    if (validate(desc, &g) != MBX_OK || slot < 0) return -1;
+    const int64_t per_row = (int64_t)g.c2 * g.s2;
+    const int64_t rows = (int64_t)(is_query ? g.c1q : g.c1k) * g.s1;
+    if (slot >= rows * per_row) return -1;
+    // slot = ((l1*s1 + r)*c2 + j1)*s2 + j
+    const int64_t j = slot % g.s2, j1 = (slot / g.s2) % g.c2, lr = slot / per_row;
+    const int l1 = (int)(lr / g.s1), r = (int)(lr % g.s1);
+    return mbx::row_base(g, is_query != 0, l1 * g.c2 + (int)j1, r) + j;
+}
 
 int mbx_selected_path(const mbx_desc* desc) {
     mbx::Geometry g;

@@ -22,7 +22,25 @@ struct Geometry {
     int64_t qs[3], ks[3], vs[3], os[3];
     const int32_t* q_order;
     const int32_t* kv_order;
+    int F, H, W;                // key grid (neighborhood plans)
+    int nf, nh, nw;             // neighborhood; nf == 0 -> identity / orders only
 };
+
+// Token row of (tile, row r, column 0) under the closed-form addressing:
+// identity slot order, or a neighborhood plan whose digits are
+// (f/nf, h/nh, nf, nh, w/nw, nw) (layout.py:319-332).  Query tiles are the last
+// c1q tile-rows of the key grid (chunked-KV), shifted to q's own frames.
+__host__ __device__ inline int64_t row_base(const Geometry& g, bool is_q, int tile, int r) {
+    const int l1 = tile / g.c2, j1 = tile - (tile / g.c2) * g.c2;
+    if (g.nf == 0) return ((int64_t)(l1 * g.s1 + r) * g.c2 + j1) * g.s2;
+    const int hcn = g.H / g.nh;
+    const int L1 = is_q ? l1 + (g.c1k - g.c1q) : l1;
+    const int fc = L1 / hcn, hc = L1 - (L1 / hcn) * hcn;
+    const int ff = r / g.nh, hf = r - (r / g.nh) * g.nh;
+    int64_t tok = ((int64_t)(fc * g.nf + ff) * g.H + hc * g.nh + hf) * g.W + j1 * g.nw;
+    if (is_q) tok -= (int64_t)((g.c1k - g.c1q) / hcn) * g.nf * g.H * g.W;
+    return tok;
+}
 
 // fp32 workspace carved out of the caller's buffer.
 struct Workspace {

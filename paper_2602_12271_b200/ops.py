@@ -105,6 +105,9 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor
     ko = _device_order(low.kv_order, q.device)
     desc.q_order = qo.data_ptr() if qo is not None else None
     desc.kv_order = ko.data_ptr() if ko is not None else None
+    if low.nbhd is not None:
+        desc.grid[:] = low.grid
+        desc.nbhd[:] = low.nbhd
     return PreparedProblem(desc, qo, ko)
 
 

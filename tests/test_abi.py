@@ -80,3 +80,36 @@ def test_forward_rejects_null_and_small_workspace(lib):
     fake = ctypes.c_void_p(16)   # never dereferenced: validation fails first
     st = lib.mbx_forward(ctypes.byref(d), fake, fake, fake, fake, None, None, fake, 1, None)
     assert st == _lib.WORKSPACE
+
+
+def test_closed_form_addressing_matches_orders(lib, goldens):
+    """mbx_token_index (the tensor-core path's row addressing) reproduces the
+    plan permutation for every neighborhood / identity golden case."""
+    import numpy as np
+
+    from cases import package_lowering
+
+    manifest, _ = goldens
+    checked = 0
+    for meta in manifest:
+        low = package_lowering(meta)
+        if low.nbhd is None and (low.q_order is not None or low.kv_order is not None):
+            continue
+        d = _desc(c1_q=low.c1_q, c1_kv=low.c1_kv, c2=low.c2, s1=low.s1, s2=low.s2, head_dim=8, v_dim=8)
+        if low.nbhd is not None:
+            d.grid[:] = low.grid
+            d.nbhd[:] = low.nbhd
+        assert lib.mbx_validate(ctypes.byref(d)) == _lib.OK, lib.mbx_last_error()
+        for is_q, order, n in ((1, low.q_order, low.n_q), (0, low.kv_order, low.n_kv)):
+            ref = np.arange(n) if order is None else order
+            got = np.array([lib.mbx_token_index(ctypes.byref(d), is_q, p) for p in range(n)])
+            assert np.array_equal(got, ref), meta["name"]
+        checked += 1
+    assert checked >= 10
+
+
+def test_closed_form_rejects_inconsistent_neighborhood(lib):
+    d = _desc()
+    d.grid[:] = (3, 30, 52)
+    d.nbhd[:] = (1, 30, 26)          # would need c2 = 2, s2 = 26
+    assert lib.mbx_validate(ctypes.byref(d)) == _lib.BAD_PLAN

@@ -172,6 +172,26 @@ def test_factors_row_stochastic_on_device(cuda):
     assert (lf.sum(dim=(4, 5, 8)) - 1).abs().max().item() < 1e-5
 
 
+@pytest.mark.parametrize("frames,q_frames,B,H", [(3, 3, 1, 12), (5, 3, 2, 2), (21, 3, 1, 1)])
+def test_tensor_core_path(cuda, frames, q_frames, B, H):
+    """The tcgen05 path is the one selected for the hot shapes and matches both
+    the oracle (2e-2) and the SIMT path run on the same inputs."""
+    g = torch.Generator(device="cpu").manual_seed(frames)
+    h, w = 30, 52
+    q = torch.randn(B, H, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k = torch.randn(B, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    v = torch.randn(B, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    plan = _sf_plan(frames, h, w)
+    low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
+    assert ops.selected_path(q, k, v, low) == "tcgen05"
+    out = ops.forward(q, k, v, low)
+    ref_simt = ops.forward(q, k, v, low, force_generic=True)
+    assert orc.rel_l2(out.float().cpu().numpy(), ref_simt.float().cpu().numpy()) < 1e-2
+    nh = min(H, 2)
+    ref = _oracle_heads(q[:1, :nh], k[:1, :nh], v[:1, :nh], low, 1)
+    assert orc.rel_l2(out[:1, :nh].float().cpu().numpy(), ref) < BF16_TOL
+
+
 def test_rejects_cpu_tensors():
     q = torch.zeros(1, 1, 4680, 128)
     with pytest.raises(pk.SolverError):
