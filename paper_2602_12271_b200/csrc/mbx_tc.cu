@@ -147,6 +147,8 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             float z[64];
             tmem_ld32(tmem_S + lane_off, z);
             tmem_ld32(tmem_S + lane_off + 32, z + 32);
+#pragma unroll
+            for (int i = 0; i < 64; ++i) z[i] *= g.scale;   // logits of scale*Q (solver.py:104)
             float m = -INFINITY;
 #pragma unroll
             for (int i = 0; i < 64; ++i)
@@ -330,7 +332,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, Geometry g, const __nv
         float sv[32];
         tmem_ld32(tmem_S + lane_off, sv);
 #pragma unroll
-        for (int l = 0; l < 32; ++l) sv[l] = (kv && l < g.s1) ? sv[l] - cl : -INFINITY;
+        for (int l = 0; l < 32; ++l) sv[l] = (kv && l < g.s1) ? sv[l] * g.scale - cl : -INFINITY;
         // column max over the 128 keys
 #pragma unroll
         for (int l = 0; l < 32; ++l) red[tid * 33 + l] = sv[l];
