@@ -1,0 +1,294 @@
+// Column stage (included by mbx_tc.cu).
+//
+// Item = group of 4 consecutive query columns (b, h, a, j..j+3).  The Q
+// columns are stacked on the four TMEM lane quadrants (rows 32i..32i+31 of
+// the A operand), so after
+//     MMA_S_i  S_i[(rows), key] = Qstack . aL_i^T      M=128, N=96 (one key chunk)
+// warp i (lane quadrant i) owns exactly the 32 query rows l of column i and
+// does an in-thread softmax over the keys (no cross-lane reductions); the other
+// 96 rows of S_i are discarded.  The joint softmax over (c, k) is online across
+// 96-key chunks with lazy rescaling (FA4 style: rescale only when the running
+// max grows by > 8 in log2 units).  The value product runs transposed so all
+// 128 lanes carry value dims:
+//     MMA_O_i  O^T_i[v, l] += Y_i^T . P_i^T            M=128, N=32, K=96
+// (solver.py:192-195 joint softmax with bias -c_L; factors.py:124 O = L Y).
+constexpr int kColThreads = 192;   // 6 warps: producer, MMA, 4 x softmax/output
+constexpr int kKC = 96;            // keys per chunk (S_i is 96 TMEM columns)
+constexpr int kRing = 6;           // aL / Y chunk slots
+struct ColSmem {
+    static constexpr int kQ = 0;                          // Qstack: 2 d-chunks x [128][64] (32 KB)
+    static constexpr int kSlot = 2 * kKC * 128;           // [96 keys][128 feat] as 2 x [96][64] (24 KB)
+    static constexpr int kRingOff = 32768;
+    static constexpr int kP = kRingOff + kRing * kSlot;   // P_i: 2 x [32 l][64 keys] (8 KB each)
+    static constexpr int kC = kP + 4 * 8192;              // c_L chunk per column: 4 x 96 floats (512 B pitch)
+    static constexpr int kStat = kC + 4 * 512;            // row sums [4][32], rescale [4][32], flags [4], rb[32]
+    static constexpr int kBars = kStat + 4 * 32 * 4 * 2 + 4 * 4 + 32 * 8;
+    static constexpr int kNumBars = 2 * kRing + 2 + 5 * 4 + 1;
+    static constexpr int kTmemSlot = kBars + kNumBars * 8;
+    static constexpr int kTotal = kTmemSlot + 16;
+};
+
+__global__ void __launch_bounds__(kColThreads, 1)
+tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_c,
+                const __grid_constant__ CUtensorMap tm_qc, Geometry g, __nv_bfloat16* __restrict__ out) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ColSmem::kBars);
+    uint64_t* ring_full = bars;                   // [6]
+    uint64_t* ring_empty = bars + kRing;          // [6]
+    uint64_t* q_full = bars + 2 * kRing;          // [1]
+    uint64_t* q_empty = q_full + 1;               // [1]
+    uint64_t* s_full = q_full + 2;                // [4]
+    uint64_t* s_free = s_full + 4;                // [4]  softmax i read S_i and c_L_i
+    uint64_t* p_full = s_free + 4;                // [4]
+    uint64_t* o_done = p_full + 4;                // [4]  MMA_O_i of the chunk completed
+    uint64_t* o_free = o_done + 4;                // [1]  all four O^T regions read out
+    uint64_t* c_full = o_free + 1;                // [4]  c_L chunk of column i landed
+    float* stat_sum = reinterpret_cast<float*>(smem + ColSmem::kStat);   // [4][32]
+    float* stat_fac = stat_sum + 128;                                    // [4][32]
+    int* flags = reinterpret_cast<int*>(stat_fac + 128);                 // [4]
+    int64_t* rb = reinterpret_cast<int64_t*>(flags + 4);                 // [32] row_base(a, l)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ColSmem::kTmemSlot);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    const int gpt = (g.s2 + 3) >> 2;                       // column groups per query tile
+    const int groups = g.bh * g.gq * gpt;
+    const int nch = (g.nkeys + kKC - 1) / kKC;
+    const int first = blockIdx.x, stride = gridDim.x;
+    const int my_groups = first < groups ? (groups - first + stride - 1) / stride : 0;
+
+    if (tid == 0) {
+        tma_prefetch(&tm_w);
+        tma_prefetch(&tm_c);
+        tma_prefetch(&tm_qc);
+        for (int i = 0; i < kRing; ++i) {
+            mbar_init(&ring_full[i], 1);
+            mbar_init(&ring_empty[i], 1);
+        }
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 32);
+            mbar_init(&p_full[i], 32);
+            mbar_init(&o_done[i], 1);
+            mbar_init(&c_full[i], 1);
+        }
+        mbar_init(o_free, 128);
+        fence_barrier_init();
+    }
+    if (warp == 0) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto decode = [&](int grp, int& bh, int& a, int& j0) {
+        const int jg = grp % gpt;
+        a = (grp / gpt) % g.gq;
+        bh = grp / (gpt * g.gq);
+        j0 = jg * 4;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            uint32_t n = 0;
+            for (int gi = 0; gi < my_groups; ++gi) {
+                int bh, a, j0;
+                decode(first + gi * stride, bh, a, j0);
+                mbar_wait(q_empty, (gi & 1) ^ 1);
+                mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
+                for (int i = 0; i < 4; ++i) {
+                    const int64_t tok0 = row_base(g, true, a, 0) + j0 + i;
+                    const int wcol = (int)(tok0 % g.W), wrow = (int)(tok0 / g.W);
+                    uint8_t* dst = smem + ColSmem::kQ + i * 4096;
+                    tma_load_4d(dst, &tm_qc, q_full, 0, wcol, wrow, bh);
+                    tma_load_4d(dst + 16384, &tm_qc, q_full, 64, wcol, wrow, bh);
+                }
+                const int col0 = (bh * g.gq + a) * g.s2 + j0;
+                for (int ch = 0; ch < nch; ++ch) {
+                    const int u = gi * nch + ch;
+                    const int k0 = ch * kKC;
+                    for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
+                        const int slot = n % kRing;
+                        mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
+                        if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);   // c_L_i buffer free
+                        mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
+                        uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
+                        tma_load_3d(dst, &tm_w, &ring_full[slot], 0, k0, col0 + i);
+                        tma_load_3d(dst + kKC * 128, &tm_w, &ring_full[slot], 64, k0, col0 + i);
+                        mbar_expect_tx(&c_full[i], kKC * 4u);
+                        tma_load_2d(smem + ColSmem::kC + i * 512, &tm_c, &c_full[i], k0, col0 + i);
+                    }
+                    for (int i = 0; i < 4; ++i, ++n) {   // Y_i
+                        const int slot = n % kRing;
+                        mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
+                        mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
+                        uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
+                        tma_load_3d(dst, &tm_w, &ring_full[slot], 128, k0, col0 + i);
+                        tma_load_3d(dst + kKC * 128, &tm_w, &ring_full[slot], 192, k0, col0 + i);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc_s = idesc_bf16(128, kKC, false, false);
+            const uint32_t idesc_o = idesc_bf16(128, 32, true, false);
+            const uint32_t sQ = smem_u32(smem + ColSmem::kQ);
+            uint32_t n = 0;
+            for (int gi = 0; gi < my_groups; ++gi) {
+                mbar_wait(q_full, gi & 1);
+                for (int ch = 0; ch < nch; ++ch) {
+                    const int u = gi * nch + ch;
+                    for (int i = 0; i < 4; ++i, ++n) {
+                        const int slot = n % kRing;
+                        mbar_wait(&ring_full[slot], (n / kRing) & 1);
+                        if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
+                        tc_fence_after();
+                        const uint32_t sA = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t ad = smem_desc(sQ + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+                            const uint64_t bd = smem_desc(sA + (kk >> 2) * (kKC * 128) + (kk & 3) * 32, 16, 1024, 2);
+                            mma_bf16(tmem + i * kKC, ad, bd, idesc_s, kk > 0);
+                        }
+                        mma_commit(&s_full[i]);
+                        mma_commit(&ring_empty[slot]);
+                    }
+                    if (ch == nch - 1) mma_commit(q_empty);
+                    for (int i = 0; i < 4; ++i, ++n) {
+                        const int slot = n % kRing;
+                        mbar_wait(&ring_full[slot], (n / kRing) & 1);
+                        mbar_wait(&p_full[i], u & 1);
+                        if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
+                        tc_fence_after();
+                        const uint32_t sY = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
+                        const uint32_t sP = smem_u32(smem + ColSmem::kP + i * 8192);
+#pragma unroll
+                        for (int kk = 0; kk < kKC / 16; ++kk) {
+                            const uint64_t ad = smem_desc(sY + kk * 2048, kKC * 128, 1024, 2);
+                            const uint64_t bd = smem_desc(sP + (kk >> 2) * 4096 + (kk & 3) * 32, 16, 1024, 2);
+                            mma_bf16(tmem + 4 * kKC + i * 32, ad, bd, idesc_o, ch > 0 || kk > 0);
+                        }
+                        mma_commit(&ring_empty[slot]);
+                        mma_commit(&o_done[i]);
+                    }
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------ softmax (warp i = column i) + output
+        const int quad = warp & 3;                       // column i within the group == lane quadrant
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const int l = lane;                              // query row of column i
+        const uint32_t sP = smem_u32(smem + ColSmem::kP + quad * 8192);
+        const float sl2 = g.scale * kLog2e;
+        const float* cbuf = reinterpret_cast<const float*>(smem + ColSmem::kC + quad * 512);
+        for (int gi = 0; gi < my_groups; ++gi) {
+            int bh, a, j0;
+            decode(first + gi * stride, bh, a, j0);
+            float m_run = -INFINITY, s_run = 0.f;
+            for (int ch = 0; ch < nch; ++ch) {
+                const int u = gi * nch + ch;
+                const int kvalid = min(kKC, g.nkeys - ch * kKC);
+                mbar_wait(&c_full[quad], u & 1);
+                mbar_wait(&s_full[quad], u & 1);
+                tc_fence_after();
+                float x[kKC];
+                tmem_ld32(tmem + quad * kKC + lane_off, x);
+                tmem_ld32(tmem + quad * kKC + 32 + lane_off, x + 32);
+                tmem_ld32(tmem + quad * kKC + 64 + lane_off, x + 64);
+                float mx = -INFINITY;
+#pragma unroll
+                for (int k = 0; k < kKC; ++k) {
+                    x[k] = k < kvalid ? fmaf(x[k], sl2, -cbuf[k] * kLog2e) : -INFINITY;
+                    mx = fmaxf(mx, x[k]);
+                }
+                tc_fence_before();
+                mbar_arrive(&s_free[quad]);
+                // lazy online max: keep m_run unless the chunk max exceeds it by > 8 (x 256)
+                float fac = 1.f;
+                int need = 0;
+                if (ch == 0) {
+                    m_run = mx;
+                } else if (mx > m_run + 8.f) {
+                    fac = exp2f(m_run - mx);
+                    m_run = mx;
+                    need = 1;
+                }
+                s_run *= fac;
+                if (ch > 0) {
+                    const int any = __any_sync(0xffffffffu, need);
+                    stat_fac[quad * 32 + l] = fac;
+                    if (lane == 0) flags[quad] = any;
+                    named_sync(1, 128);
+                    const int f = flags[0] | flags[1] | flags[2] | flags[3];
+                    if (f) {   // rescale O^T of every flagged column: thread = value lane
+                        for (int i = 0; i < 4; ++i) {
+                            if (!flags[i]) continue;
+                            mbar_wait(&o_done[i], (u - 1) & 1);
+                            tc_fence_after();
+                            float o[32];
+                            tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
+#pragma unroll
+                            for (int q = 0; q < 32; ++q) o[q] *= stat_fac[i * 32 + q];
+                            tmem_st32(tmem + 4 * kKC + i * 32 + lane_off, o);
+                        }
+                        tc_fence_before();
+                    }
+                    named_sync(1, 128);
+                }
+                // P_i row l (bf16, K-major SW128: keys 0-63 chunk 0, keys 64-95 chunk 1)
+                uint32_t pk[kKC / 2];
+                float sum = 0.f;
+#pragma unroll
+                for (int k = 0; k < kKC; k += 2) {
+                    const float p0 = exp2f(x[k] - m_run), p1 = exp2f(x[k + 1] - m_run);
+                    sum += p0 + p1;
+                    pk[k >> 1] = pack_bf16(p0, p1);
+                }
+                s_run += sum;
+                if (u > 0) mbar_wait(&o_done[quad], (u - 1) & 1);   // MMA_O_i(u-1) done with P_i
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc)
+                    st_shared_v4(sP + l * 128 + ((cc ^ (l & 7)) << 4), pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2],
+                                 pk[4 * cc + 3]);
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc)
+                    st_shared_v4(sP + 4096 + l * 128 + ((cc ^ (l & 7)) << 4), pk[32 + 4 * cc], pk[33 + 4 * cc],
+                                 pk[34 + 4 * cc], pk[35 + 4 * cc]);
+                fence_proxy_async_smem();
+                mbar_arrive(&p_full[quad]);
+            }
+            // ---- output of the 4 columns: O[l, v] = O^T_i[v, l] / s_l ----
+            stat_sum[quad * 32 + l] = s_run;
+            if (warp == 2) rb[l] = l < g.s1 ? row_base(g, true, a, l) : 0;
+            named_sync(1, 128);
+            const int v = quad * 32 + lane;              // this thread's TMEM lane = value dim
+            const int b = bh / g.heads, h = bh % g.heads;
+            __nv_bfloat16* ob = out + b * g.os[0] + h * g.os[1];
+            const int ulast = gi * nch + nch - 1;
+            for (int i = 0; i < 4; ++i) {
+                mbar_wait(&o_done[i], ulast & 1);
+                tc_fence_after();
+                float o[32];
+                tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
+                const int j = j0 + i;
+                if (j < g.s2) {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        if (q < g.s1) ob[(rb[q] + j) * g.os[2] + v] = __float2bfloat16_rn(o[q] / stat_sum[i * 32 + q]);
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(o_free);
+            named_sync(1, 128);   // stat_sum / rb reused by the next group
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
