@@ -20,10 +20,10 @@ struct ColSmem {
     static constexpr int kSlot = 2 * kKC * 128;           // [96 keys][128 feat] as 2 x [96][64] (24 KB)
     static constexpr int kRingOff = 32768;
     static constexpr int kP = kRingOff + kRing * kSlot;   // P_i: 2 x [32 l][64 keys] (8 KB each)
-    static constexpr int kC = kP + 4 * 8192;              // c_L chunk per column: 4 x 96 floats (512 B pitch)
-    static constexpr int kStat = kC + 4 * 512;            // row sums [4][32], rescale [4][32], flags [4], rb[32]
+    static constexpr int kC = kP + 4 * 8192;              // c_L chunks: [4 columns][2 buffers] x 96 floats (512 B pitch)
+    static constexpr int kStat = kC + 8 * 512;            // row sums [4][32], rescale [4][32], flags [4], rb[32]
     static constexpr int kBars = kStat + 4 * 32 * 4 * 2 + 4 * 4 + 32 * 8;
-    static constexpr int kNumBars = 2 * kRing + 2 + 5 * 4 + 1;
+    static constexpr int kNumBars = 2 * kRing + 2 + 4 * 4 + 1 + 16;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
@@ -43,7 +43,8 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
     uint64_t* p_full = s_free + 4;                // [4]
     uint64_t* o_done = p_full + 4;                // [4]  MMA_O_i of the chunk completed
     uint64_t* o_free = o_done + 4;                // [1]  all four O^T regions read out
-    uint64_t* c_full = o_free + 1;                // [4]  c_L chunk of column i landed
+    uint64_t* c_full = o_free + 1;                // [4][2]  c_L chunk of column i landed
+    uint64_t* c_empty = c_full + 8;               // [4][2]  softmax i read it
     float* stat_sum = reinterpret_cast<float*>(smem + ColSmem::kStat);   // [4][32]
     float* stat_fac = stat_sum + 128;                                    // [4][32]
     int* flags = reinterpret_cast<int*>(stat_fac + 128);                 // [4]
@@ -72,7 +73,10 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             mbar_init(&s_free[i], 32);
             mbar_init(&p_full[i], 32);
             mbar_init(&o_done[i], 1);
+        }
+        for (int i = 0; i < 8; ++i) {
             mbar_init(&c_full[i], 1);
+            mbar_init(&c_empty[i], 32);
         }
         mbar_init(o_free, 128);
         fence_barrier_init();
@@ -113,13 +117,14 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
                         const int slot = n % kRing;
                         mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);   // c_L_i buffer free
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_3d(dst, &tm_w, &ring_full[slot], 0, k0, col0 + i);
                         tma_load_3d(dst + kKC * 128, &tm_w, &ring_full[slot], 64, k0, col0 + i);
-                        mbar_expect_tx(&c_full[i], kKC * 4u);
-                        tma_load_2d(smem + ColSmem::kC + i * 512, &tm_c, &c_full[i], k0, col0 + i);
+                        const int cb = i * 2 + (u & 1);
+                        mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
+                        mbar_expect_tx(&c_full[cb], kKC * 4u);
+                        tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
                     }
                     for (int i = 0; i < 4; ++i, ++n) {   // Y_i
                         const int slot = n % kRing;
@@ -186,7 +191,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         const int l = lane;                              // query row of column i
         const uint32_t sP = smem_u32(smem + ColSmem::kP + quad * 8192);
         const float sl2 = g.scale * kLog2e;
-        const float* cbuf = reinterpret_cast<const float*>(smem + ColSmem::kC + quad * 512);
+
         for (int gi = 0; gi < my_groups; ++gi) {
             int bh, a, j0;
             decode(first + gi * stride, bh, a, j0);
@@ -194,7 +199,9 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             for (int ch = 0; ch < nch; ++ch) {
                 const int u = gi * nch + ch;
                 const int kvalid = min(kKC, g.nkeys - ch * kKC);
-                mbar_wait(&c_full[quad], u & 1);
+                const int cb = quad * 2 + (u & 1);
+                const float* cbuf = reinterpret_cast<const float*>(smem + ColSmem::kC + cb * 512);
+                mbar_wait(&c_full[cb], (u >> 1) & 1);
                 mbar_wait(&s_full[quad], u & 1);
                 tc_fence_after();
                 float x[kKC];
@@ -209,6 +216,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 }
                 tc_fence_before();
                 mbar_arrive(&s_free[quad]);
+                mbar_arrive(&c_empty[cb]);
                 // lazy online max: keep m_run unless the chunk max exceeds it by > 8 (x 256)
                 float fac = 1.f;
                 int need = 0;
