@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmonarch_b200.so")
+LIB_PATH = os.environ.get("MBX_LIB") or os.path.join(HERE, "libmonarch_b200.so")
 
 ABI_VERSION = 1
 F32, BF16 = 0, 1

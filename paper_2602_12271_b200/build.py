@@ -37,8 +37,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds libmonarch_b200_trace.so with per-CTA event timestamps
+    (MBX_TRACE; a profiling aid, never loaded unless MBX_LIB points at it)."""
+    lib = LIB.replace(".so", "_trace.so") if trace else LIB
+    if not force and not trace and not _stale():
         return LIB
     objs = []
     tmp = os.path.join(HERE, "_build")
@@ -47,16 +50,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
                     "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if trace:
+        flags += ["-DMBX_TRACE"]
     for src in SOURCES:
-        obj = os.path.join(tmp, src.replace(".cu", ".o"))
+        obj = os.path.join(tmp, src.replace(".cu", "_trace.o" if trace else ".o"))
         cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", obj] + flags
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp_lib = LIB + ".tmp"
+    tmp_lib = lib + ".tmp"
     subprocess.run([nvcc(), "-shared", "-o", tmp_lib] + objs + ARCH + ["-lcuda"], check=True)
-    os.replace(tmp_lib, LIB)
-    return LIB
+    os.replace(tmp_lib, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

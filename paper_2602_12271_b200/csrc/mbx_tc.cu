@@ -22,13 +22,29 @@ using namespace sm100;
 constexpr int kD = 128;           // head dim (q, k) and value dim
 constexpr int kMaxS2 = 64;        // tile-row tokens (MMA1 N, MMA2 K)
 constexpr int kMaxS1 = 32;        // tile rows (column-stage N)
-constexpr int kMaxGq = 4;         // query tiles per key row (2 M tiles)
+constexpr int kMaxGq = 3;         // query tiles per key row (M tile 0: a=0,1; M tile 1: a=2)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t ring_parity(uint32_t n, uint32_t size) { return (n / size) & 1u; }
 
 // c_L rows are padded to 32 floats so each column's row is a 16-byte aligned TMA box.
 __host__ __device__ __forceinline__ int ckey_stride(const Geometry& g) { return (g.nkeys + 31) & ~31; }
+
+#ifdef MBX_TRACE
+// Event timestamps of the first kTraceCtas CTAs: [cta][role][event] = (globaltimer << 8) | tag.
+constexpr int kTraceCtas = 4, kTraceRoles = 8, kTraceEvents = 4096;
+__device__ unsigned long long g_trace[kTraceCtas][kTraceRoles][kTraceEvents];
+__device__ __forceinline__ void trace_ev(int role, int& idx, int tag) {
+    if (blockIdx.x < kTraceCtas && idx < kTraceEvents) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace[blockIdx.x][role][idx++] = (t << 8) | (unsigned)tag;
+    }
+}
+#define TR(role, idx, tag) trace_ev(role, idx, tag)
+#else
+#define TR(role, idx, tag) ((void)0)
+#endif
 
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
@@ -139,7 +155,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
         return cudaErrorInvalidValue;
-    CUtensorMap tq, tk, tv, tqc, tw, tc;
+    CUtensorMap tq, tk, tv, tqc, tw, tws, tc;
     if (!make_rows_map(&tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&tk, k, B, g.heads, nk, g.ks, g.s2) ||
         !make_rows_map(&tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&tqc, q, g, nq))
         return cudaErrorInvalidValue;
@@ -148,10 +164,14 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(workspace);
     float* Wc = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256(rows * 512));
     {
-        cuuint64_t dims[3] = {256, (cuuint64_t)g.nkeys, (cuuint64_t)ncols};
-        cuuint64_t strides[2] = {512, (cuuint64_t)g.nkeys * 512};
-        cuuint32_t box[3] = {64, (cuuint32_t)kKC, 1};
-        if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        // blocked W[col][part][key][64]: part 0,1 = aL halves, 2,3 = Y halves
+        cuuint64_t dims[4] = {64, (cuuint64_t)g.nkeys, 4, (cuuint64_t)ncols};
+        cuuint64_t strides[3] = {128, (cuuint64_t)g.nkeys * 128, (cuuint64_t)g.nkeys * 512};
+        cuuint32_t box[4] = {64, (cuuint32_t)kKC, 1, 1};          // column stage: contiguous 12 KB
+        if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+        cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)g.s2};          // row stage: one key, s2 columns
+        if (!encode(&tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
@@ -172,7 +192,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int grid_row = items < num_sms() ? items : num_sms();
     {
         ProfScope p("tc_row_stage", stream);
-        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(tq, tk, tv, g, Wp, Wc);
+        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(tq, tk, tv, tws, g, Wc);
     }
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
     const int grid_col = ngroups < num_sms() ? (int)ngroups : num_sms();
@@ -185,3 +205,15 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
 }
 
 }  // namespace mbx
+
+#ifdef MBX_TRACE
+extern "C" int mbx_trace_dump(void* host, size_t bytes) {
+    if (bytes < sizeof(mbx::g_trace)) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host, mbx::g_trace, sizeof(mbx::g_trace));
+    cudaMemset(reinterpret_cast<void*>(0), 0, 0);
+    static unsigned long long zeros[4 * 8 * 4096];
+    cudaMemcpyToSymbol(mbx::g_trace, zeros, sizeof(zeros));
+    return (int)sizeof(mbx::g_trace);
+}
+#endif

@@ -1,17 +1,37 @@
-// =============================================================== row stage
+// Row stage (included by mbx_tc.cu).
+//
+// Item = (b, h, in-tile row k): the Q rows k of all query tiles stay in smem
+// while the K/V rows k of every key tile c stream through a 2-stage TMA ring.
+// Per task (c, M-tile of two query tiles):
+//   MMA1  S[(a,j), i] = Q_k . K_ck^T        128 x 64 x 128      -> TMEM buffer t%2
+//   softmax_i (warps 2-5, one query row per thread), c_L = sum R z - lse
+//   MMA2  [aL | Y]    = P . [K_ck | V_ck]   128 x 256 x 64      -> same TMEM buffer
+//   epilogue (warps 6-9): * 1/l, bf16, staged in smem, TMA-stored to the blocked
+//   workspace W[col][part][key][64] (part 0,1 = aL halves, 2,3 = Y halves), so the
+//   column stage reads contiguous 12 KB boxes.  (solver.py:187-191, factors.py:123)
 constexpr int kRowThreads = 320;   // 10 warps
 struct RowSmem {
-    static constexpr int kQ = 0;                      // Q[2]: 2 M tiles x 2 d-chunks x [128][64]  (64 KB each)
-    static constexpr int kQBytes = 65536;
+    // Q[2] (48 KB each): query tile a < 2 -> d-chunk c at c*16K + a*8K (M tile 0 rows a*64..);
+    // a == 2 -> M tile 1 at 32K + c*8K (its rows 64..127 read the next 8 KB: discarded rows).
+    static constexpr int kQ = 0;
+    static constexpr int kQBytes = 49152;
     static constexpr int kKV = 2 * kQBytes;           // KV[2]: [K c0 | K c1 | V c0 | V c1] 8 KB each (32 KB)
     static constexpr int kKVBytes = 32768;
     static constexpr int kP = kKV + 2 * kKVBytes;     // P: [128][64] bf16 (16 KB)
-    static constexpr int kStats = kP + 16384;         // stats[2][128] float2 (inv_l, c_L)
+    static constexpr int kStage = kP + 16384;         // epilogue staging [2] x [128][64] bf16 (16 KB each)
+    static constexpr int kStats = kStage + 2 * 16384; // stats[2][128] float2 (inv_l, c_L)
     static constexpr int kBars = kStats + 2 * 128 * 8;
     static constexpr int kNumBars = 16;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
+
+__host__ __device__ __forceinline__ int q_slot_off(int a, int c) {
+    return a < 2 ? c * 16384 + a * 8192 : 32768 + c * 8192;
+}
+__host__ __device__ __forceinline__ int q_tile_off(int mt, int c) {
+    return mt == 0 ? c * 16384 : 32768 + c * 8192;
+}
 
 struct RowTask {            // decoded task t of this CTA
     int item, c, mt;
@@ -32,9 +52,21 @@ __device__ __forceinline__ RowTask row_task(int t, int n_mt, int gk, int first_i
     return r;
 }
 
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+
 __global__ void __launch_bounds__(kRowThreads, 1)
 tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-             const __grid_constant__ CUtensorMap tm_v, Geometry g, __nv_bfloat16* __restrict__ W,
+             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_wst, Geometry g,
              float* __restrict__ Wc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -63,6 +95,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
+        tma_prefetch(&tm_wst);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
@@ -76,8 +109,8 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         mbar_init(p_empty, 1);
         fence_barrier_init();
     }
-    // rows s2..63 of every K/V/Q box slot (and unused query-tile slots) are never
-    // written by TMA (box = s2 rows): zero them once so MMA padding reads zeros.
+    // Rows s2..63 of every box slot are never written by TMA (box = s2 rows): zero
+    // the operand buffers once so MMA padding rows/keys read zeros.
     for (int i = tid; i < (2 * RowSmem::kQBytes + 2 * RowSmem::kKVBytes) / 16; i += kRowThreads)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -102,9 +135,8 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                     uint8_t* qb = smem + RowSmem::kQ + qs * RowSmem::kQBytes;
                     for (int a = 0; a < g.gq; ++a) {
                         const int tok = (int)row_base(g, true, a, kr);
-                        uint8_t* dst = qb + (a >> 1) * 32768 + (a & 1) * 8192;
-                        tma_load_4d(dst, &tm_q, &q_full[qs], 0, tok, h, b);
-                        tma_load_4d(dst + 16384, &tm_q, &q_full[qs], 64, tok, h, b);
+                        tma_load_4d(qb + q_slot_off(a, 0), &tm_q, &q_full[qs], 0, tok, h, b);
+                        tma_load_4d(qb + q_slot_off(a, 1), &tm_q, &q_full[qs], 64, tok, h, b);
                     }
                     ++nq;
                 }
@@ -129,44 +161,40 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const uint32_t idesc_o = idesc_bf16(128, 256, false, true);
             const uint32_t p_base = smem_u32(smem + RowSmem::kP);
             uint32_t nq = 0, nkv = 0;
-            // MMA1 for task t (needs Q, K/V and a free TMEM buffer)
-            auto issue_s = [&](int t, const RowTask& tk) {
+            auto issue_s = [&](int t, const RowTask& tk) {   // MMA1 for task t
                 const int qs = (nq - 1) & 1, ks = (nkv - 1) & 1;
                 const int bsel = t & 1;
                 mbar_wait(&t_empty[bsel], ring_parity(t, 2) ^ 1);
                 tc_fence_after();
-                const uint32_t qbase = smem_u32(smem + RowSmem::kQ + qs * RowSmem::kQBytes) + tk.mt * 32768;
+                const uint32_t qbase = smem_u32(smem + RowSmem::kQ + qs * RowSmem::kQBytes);
                 const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = smem_desc(qbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
+                    const uint64_t ad = smem_desc(qbase + q_tile_off(tk.mt, kk >> 2) + (kk & 3) * 32, 16, 1024, 2);
                     const uint64_t bd = smem_desc(kbase + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2);
                     mma_bf16(tmem + bsel * 256, ad, bd, idesc_s, kk > 0);
                 }
                 mma_commit(&s_full[bsel]);
             };
-            RowTask cur{};
             for (int t = 0; t < my_tasks; ++t) {
-                cur = row_task(t, n_mt, g.gk, first_item, item_stride);
+                const RowTask cur = row_task(t, n_mt, g.gk, first_item, item_stride);
                 if (t == 0) {
                     if (cur.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; }
                     if (cur.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; }
                     issue_s(t, cur);
                 }
                 // look ahead: MMA1(t+1) before MMA2(t) so it overlaps softmax(t)
+                int adv = 0, advq = 0;
                 if (t + 1 < my_tasks) {
                     const RowTask nx = row_task(t + 1, n_mt, g.gk, first_item, item_stride);
-                    if (nx.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; }
-                    if (nx.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; }
+                    if (nx.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; advq = 1; }
+                    if (nx.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; adv = 1; }
                     issue_s(t + 1, nx);
                 }
                 // MMA2(t): [aL | Y] = P . [K | V]
                 const int bsel = t & 1;
                 mbar_wait(p_full, ring_parity(t, 1));
                 tc_fence_after();
-                // K/V stage of task t: stage of its c (tasks t+1 may have advanced nkv)
-                const int adv = (t + 1 < my_tasks) &&
-                                row_task(t + 1, n_mt, g.gk, first_item, item_stride).first_of_c;
                 const int ks = (nkv - 1 - adv) & 1;
                 const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
 #pragma unroll
@@ -178,11 +206,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 mma_commit(&o_full[bsel]);
                 mma_commit(p_empty);
                 if (cur.last_of_c) mma_commit(&kv_empty[ks]);
-                if (cur.last_of_item) {
-                    const int advq = (t + 1 < my_tasks) &&
-                                     row_task(t + 1, n_mt, g.gk, first_item, item_stride).first_of_item;
-                    mma_commit(&q_empty[(nq - 1 - advq) & 1]);
-                }
+                if (cur.last_of_item) mma_commit(&q_empty[(nq - 1 - advq) & 1]);
             }
         }
     } else if (warp < 6) {
@@ -221,8 +245,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             }
             const float inv_l = 1.f / l;
             // c_L = sum R z - lse with z = scale * S
-            const float c_l = g.scale * (A * inv_l - m) - __logf(l);
-            stats[bsel * 128 + r] = make_float2(inv_l, c_l);
+            stats[bsel * 128 + r] = make_float2(inv_l, g.scale * (A * inv_l - m) - __logf(l));
             tc_fence_before();
             mbar_wait(p_empty, ring_parity(t, 1) ^ 1);
 #pragma unroll
@@ -233,46 +256,59 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             mbar_arrive(p_full);
         }
     } else {
-        // ------------------------------------------------------ epilogue
+        // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const bool leader = (warp == 6 && lane == 0);
+        int nstore = 0;   // staging buffer uses
         for (int t = 0; t < my_tasks; ++t) {
             const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
             const int bsel = t & 1;
             const int a = tk.mt * 2 + (r >> 6), j = r & 63;
             const bool row_ok = a < g.gq && j < g.s2;
             const int kr = tk.item % g.s1, bh = tk.item / g.s1;
+            const int key = tk.c * g.s1 + kr;
             mbar_wait(&o_full[bsel], ring_parity(t, 2));
             tc_fence_after();
             const float2 st = stats[bsel * 128 + r];
-            const int64_t wrow = (((int64_t)bh * g.gq + (row_ok ? a : 0)) * g.s2 + (row_ok ? j : 0)) * g.nkeys +
-                                 tk.c * g.s1 + kr;
-            uint4* dst = reinterpret_cast<uint4*>(W + wrow * 256);
+            for (int part = 0; part < 4; ++part, ++nstore) {
+                const int sb = nstore & 1;
+                float o[64];
+                tmem_ld32(tmem + bsel * 256 + lane_off + part * 64, o);
+                tmem_ld32(tmem + bsel * 256 + lane_off + part * 64 + 32, o + 32);
+                if (part == 3) {   // TMEM buffer fully read: MMA1(t+2) may reuse it
+                    tc_fence_before();
+                    mbar_arrive(&t_empty[bsel]);
+                }
+                // staging buffer sb must have been read by its previous TMA store
+                if (leader) bulk_wait_read<1>();
+                named_sync(2, 128);
+                const uint32_t srow = smem_u32(smem + RowSmem::kStage + sb * 16384) + r * 128;
 #pragma unroll
-            for (int q32 = 0; q32 < 8; ++q32) {
-                float o[32];
-                tmem_ld32(tmem + bsel * 256 + lane_off + q32 * 32, o);
-                if (row_ok) {
-#pragma unroll
-                    for (int v4 = 0; v4 < 4; ++v4) {
-                        uint4 pk;
-                        pk.x = pack_bf16(o[8 * v4 + 0] * st.x, o[8 * v4 + 1] * st.x);
-                        pk.y = pack_bf16(o[8 * v4 + 2] * st.x, o[8 * v4 + 3] * st.x);
-                        pk.z = pack_bf16(o[8 * v4 + 4] * st.x, o[8 * v4 + 5] * st.x);
-                        pk.w = pack_bf16(o[8 * v4 + 6] * st.x, o[8 * v4 + 7] * st.x);
-                        dst[q32 * 4 + v4] = pk;
+                for (int cc = 0; cc < 8; ++cc)
+                    st_shared_v4(srow + ((cc ^ (r & 7)) << 4),
+                                 pack_bf16(o[8 * cc] * st.x, o[8 * cc + 1] * st.x),
+                                 pack_bf16(o[8 * cc + 2] * st.x, o[8 * cc + 3] * st.x),
+                                 pack_bf16(o[8 * cc + 4] * st.x, o[8 * cc + 5] * st.x),
+                                 pack_bf16(o[8 * cc + 6] * st.x, o[8 * cc + 7] * st.x));
+                fence_proxy_async_smem();
+                named_sync(2, 128);
+                if (leader) {
+                    for (int qa = 0; qa < 2; ++qa) {
+                        const int aa = tk.mt * 2 + qa;
+                        if (aa >= g.gq) break;
+                        tma_store_4d(&tm_wst, smem + RowSmem::kStage + sb * 16384 + qa * 8192, 0, key, part,
+                                     (bh * g.gq + aa) * g.s2);
                     }
+                    bulk_commit();
                 }
             }
-            if (row_ok)
-                Wc[(((int64_t)bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + tk.c * g.s1 + kr] = st.y;
-            tc_fence_before();
-            mbar_arrive(&t_empty[bsel]);
+            if (row_ok) Wc[(((int64_t)bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = st.y;
         }
+        if (leader) bulk_wait<0>();
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
 }
-
