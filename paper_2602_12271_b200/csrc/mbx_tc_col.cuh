@@ -214,7 +214,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 const int u = gi * nch + ch;
                 const int kvalid = min(kKC, g.nkeys - ch * kKC);
                 const int cb = quad * 2 + (u & 1);
-                const float* cbuf = reinterpret_cast<const float*>(smem + ColSmem::kC + cb * 512);
+                const uint32_t cbuf = smem_u32(smem + ColSmem::kC + cb * 512);
                 mbar_wait(&c_full[cb], (u >> 1) & 1);
                 if (lane == 0) TR(warp, ti, 21);
                 mbar_wait(&s_full[quad], u & 1);
@@ -226,9 +226,15 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 tmem_ld32(tmem + quad * kKC + 64 + lane_off, x + 64);
                 float mx = -INFINITY;
 #pragma unroll
-                for (int k = 0; k < kKC; ++k) {
-                    x[k] = k < kvalid ? fmaf(x[k], sl2, -cbuf[k] * kLog2e) : -INFINITY;
-                    mx = fmaxf(mx, x[k]);
+                for (int k4 = 0; k4 < kKC; k4 += 4) {
+                    const float4 c4 = ld_shared_v4f(cbuf + k4 * 4);
+                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int k = k4 + e;
+                        x[k] = k < kvalid ? fmaf(x[k], sl2, -cv[e] * kLog2e) : -INFINITY;
+                        mx = fmaxf(mx, x[k]);
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(&s_free[quad]);
@@ -289,12 +295,15 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 if (lane == 0) TR(warp, ti, 23);
             }
             // ---- output of the 4 columns: O[l, v] = O^T_i[v, l] / s_l ----
-            stat_sum[quad * 32 + l] = s_run;
-            if (warp == 2) rb[l] = l < g.s1 ? row_base(g, true, a, l) : 0;
+            // tile rows are contiguous W-token grid rows: token(l, j) = row_base(a,0) + j + l*W
+            const uint32_t sinv = smem_u32(stat_sum);
+            st_shared_f32(sinv + (quad * 32 + l) * 4, 1.f / s_run);
             named_sync(1, 128);
             const int v = quad * 32 + lane;              // this thread's TMEM lane = value dim
             const int b = bh / g.heads, h = bh % g.heads;
-            __nv_bfloat16* ob = out + b * g.os[0] + h * g.os[1];
+            __nv_bfloat16* ob = out + b * g.os[0] + h * g.os[1] + v;
+            const int64_t tok0 = row_base(g, true, a, 0) + j0;
+            const int64_t lstep = (int64_t)g.W * g.os[2];
             const int ulast = gi * nch + nch - 1;
             if (lane == 0) TR(warp, ti, 25);
             for (int i = 0; i < 4; ++i) {
@@ -303,11 +312,17 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 tc_fence_after();
                 float o[32];
                 tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
-                const int j = j0 + i;
-                if (j < g.s2) {
+                float inv[32];
+#pragma unroll
+                for (int q4 = 0; q4 < 32; q4 += 4) {
+                    const float4 t4 = ld_shared_v4f(sinv + (i * 32 + q4) * 4);
+                    inv[q4] = t4.x; inv[q4 + 1] = t4.y; inv[q4 + 2] = t4.z; inv[q4 + 3] = t4.w;
+                }
+                if (j0 + i < g.s2) {
+                    __nv_bfloat16* col = ob + (tok0 + i) * g.os[2];
 #pragma unroll
                     for (int q = 0; q < 32; ++q)
-                        if (q < g.s1) ob[(rb[q] + j) * g.os[2] + v] = __float2bfloat16_rn(o[q] / stat_sum[i * 32 + q]);
+                        if (q < g.s1) col[q * lstep] = __float2bfloat16_rn(o[q] * inv[q]);
                 }
             }
             tc_fence_before();
