@@ -124,6 +124,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
             uint32_t nq = 0, nkv = 0;
+            int ti = 0;
             for (int t = 0; t < my_tasks; ++t) {
                 const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
                 const int kr = tk.item % g.s1, bh = tk.item / g.s1;
@@ -131,6 +132,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 if (tk.first_of_item) {
                     const int qs = nq & 1;
                     mbar_wait(&q_empty[qs], ring_parity(nq, 2) ^ 1);
+                    TR(0, ti, 1);
                     mbar_expect_tx(&q_full[qs], 2u * box_bytes * (uint32_t)g.gq);
                     uint8_t* qb = smem + RowSmem::kQ + qs * RowSmem::kQBytes;
                     for (int a = 0; a < g.gq; ++a) {
@@ -143,6 +145,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 if (tk.first_of_c) {
                     const int ks = nkv & 1;
                     mbar_wait(&kv_empty[ks], ring_parity(nkv, 2) ^ 1);
+                    TR(0, ti, 2);
                     mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
                     uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
                     const int tok = (int)row_base(g, false, tk.c, kr);
@@ -161,10 +164,12 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const uint32_t idesc_o = idesc_bf16(128, 256, false, true);
             const uint32_t p_base = smem_u32(smem + RowSmem::kP);
             uint32_t nq = 0, nkv = 0;
+            int ti = 0;
             auto issue_s = [&](int t, const RowTask& tk) {   // MMA1 for task t
                 const int qs = (nq - 1) & 1, ks = (nkv - 1) & 1;
                 const int bsel = t & 1;
                 mbar_wait(&t_empty[bsel], ring_parity(t, 2) ^ 1);
+                TR(1, ti, 11);
                 tc_fence_after();
                 const uint32_t qbase = smem_u32(smem + RowSmem::kQ + qs * RowSmem::kQBytes);
                 const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
@@ -194,6 +199,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 // MMA2(t): [aL | Y] = P . [K | V]
                 const int bsel = t & 1;
                 mbar_wait(p_full, ring_parity(t, 1));
+                TR(1, ti, 12);
                 tc_fence_after();
                 const int ks = (nkv - 1 - adv) & 1;
                 const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
@@ -216,12 +222,14 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t p_row = smem_u32(smem + RowSmem::kP) + r * 128;
         const float sl2 = g.scale * kLog2e;
+        int ti = 0;
         for (int t = 0; t < my_tasks; ++t) {
             const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
             const int bsel = t & 1;
             const int a = tk.mt * 2 + (r >> 6), j = r & 63;
             const bool row_ok = a < g.gq && j < g.s2;
             mbar_wait(&s_full[bsel], ring_parity(t, 2));
+            if (lane == 0) TR(warp, ti, 21);
             tc_fence_after();
             float z[64];
             tmem_ld32(tmem + bsel * 256 + lane_off, z);
@@ -254,6 +262,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                              packed[4 * cc + 2], packed[4 * cc + 3]);
             fence_proxy_async_smem();
             mbar_arrive(p_full);
+            if (lane == 0) TR(warp, ti, 22);
         }
     } else {
         // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
@@ -262,6 +271,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const bool leader = (warp == 6 && lane == 0);
         int nstore = 0;   // staging buffer uses
+        int ti = 0;
         for (int t = 0; t < my_tasks; ++t) {
             const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
             const int bsel = t & 1;
@@ -270,6 +280,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const int kr = tk.item % g.s1, bh = tk.item / g.s1;
             const int key = tk.c * g.s1 + kr;
             mbar_wait(&o_full[bsel], ring_parity(t, 2));
+            if (lane == 0 && warp < 8) TR(warp, ti, 31);
             tc_fence_after();
             const float2 st = stats[bsel * 128 + r];
             for (int part = 0; part < 4; ++part, ++nstore) {
@@ -305,6 +316,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 }
             }
             if (row_ok) Wc[(((int64_t)bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = st.y;
+            if (lane == 0 && warp < 8) TR(warp, ti, 32);
         }
         if (leader) bulk_wait<0>();
     }

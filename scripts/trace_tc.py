@@ -26,7 +26,7 @@ for it in range(3):
     torch.cuda.synchronize()
     lib.mbx_trace_dump(buf.ctypes.data, buf.nbytes)   # keep only the last run's trace
 ev = buf.reshape(4, 8, 4096)
-for cta in range(1):
+for cta in range(int(os.environ.get("NCTA", "1"))):
     allt = [int(x) >> 8 for x in ev[cta].ravel() if x]
     t0 = min(allt) if allt else 0
     for role in range(8):
