@@ -32,7 +32,7 @@ __host__ __device__ __forceinline__ int ckey_stride(const Geometry& g) { return 
 
 #ifdef MBX_TRACE
 // Event timestamps of the first kTraceCtas CTAs: [cta][role][event] = (globaltimer << 8) | tag.
-constexpr int kTraceCtas = 4, kTraceRoles = 8, kTraceEvents = 4096;
+constexpr int kTraceCtas = 4, kTraceRoles = 16, kTraceEvents = 2048;
 __device__ unsigned long long g_trace[kTraceCtas][kTraceRoles][kTraceEvents];
 __device__ __forceinline__ void trace_ev(int role, int& idx, int tag) {
     if (blockIdx.x < kTraceCtas && idx < kTraceEvents) {
@@ -155,7 +155,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
         return cudaErrorInvalidValue;
-    CUtensorMap tq, tk, tv, tqc, tw, tws, tc;
+    CUtensorMap tq, tk, tv, tqc, tw, tws, tws_b, tc;
     if (!make_rows_map(&tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&tk, k, B, g.heads, nk, g.ks, g.s2) ||
         !make_rows_map(&tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&tqc, q, g, nq))
         return cudaErrorInvalidValue;
@@ -170,8 +170,12 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t box[4] = {64, (cuuint32_t)kKC, 1, 1};          // column stage: contiguous 12 KB
         if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
-        cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)g.s2};          // row stage: one key, s2 columns
+        // row stage: one key, the columns j of one epilogue warp (rows 0..31 and 32..s2-1)
+        cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 32 ? g.s2 : 32)};
         if (!encode(&tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+        cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
+        if (!encode(&tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
@@ -192,7 +196,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int grid_row = items < num_sms() ? items : num_sms();
     {
         ProfScope p("tc_row_stage", stream);
-        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(tq, tk, tv, tws, g, Wc);
+        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(tq, tk, tv, tws, tws_b, g, Wc);
     }
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
     const int grid_col = ngroups < num_sms() ? (int)ngroups : num_sms();
@@ -212,7 +216,7 @@ extern "C" int mbx_trace_dump(void* host, size_t bytes) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(host, mbx::g_trace, sizeof(mbx::g_trace));
     cudaMemset(reinterpret_cast<void*>(0), 0, 0);
-    static unsigned long long zeros[4 * 8 * 4096];
+    static unsigned long long zeros[4 * 16 * 2048];
     cudaMemcpyToSymbol(mbx::g_trace, zeros, sizeof(zeros));
     return (int)sizeof(mbx::g_trace);
 }

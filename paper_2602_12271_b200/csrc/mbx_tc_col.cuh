@@ -103,7 +103,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 int bh, a, j0;
                 decode(first + gi * stride, bh, a, j0);
                 mbar_wait(q_empty, (gi & 1) ^ 1);
-                TR(0, ti, 5);
+                TR(8, ti, 5);
                 mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
                 for (int i = 0; i < 4; ++i) {
                     const int64_t tok0 = row_base(g, true, a, 0) + j0 + i;
@@ -118,24 +118,24 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     const int k0 = ch * kKC;
                     for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
                         const int slot = n % kRing;
-                        TR(0, ti, 1);
+                        TR(8, ti, 1);
                         mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TR(0, ti, 2);
+                        TR(8, ti, 2);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
                         tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
                         const int cb = i * 2 + (u & 1);
                         mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
-                        TR(0, ti, 4);
+                        TR(8, ti, 4);
                         mbar_expect_tx(&c_full[cb], kKC * 4u);
                         tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
                     }
                     for (int i = 0; i < 4; ++i, ++n) {   // Y_i
                         const int slot = n % kRing;
-                        TR(0, ti, 6);
+                        TR(8, ti, 6);
                         mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TR(0, ti, 7);
+                        TR(8, ti, 7);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0 + i);
@@ -154,15 +154,15 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             int ti = 0;
             for (int gi = 0; gi < my_groups; ++gi) {
                 mbar_wait(q_full, gi & 1);
-                TR(1, ti, 16);
+                TR(9, ti, 16);
                 for (int ch = 0; ch < nch; ++ch) {
                     const int u = gi * nch + ch;
                     for (int i = 0; i < 4; ++i, ++n) {
                         const int slot = n % kRing;
                         mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TR(1, ti, 11);
+                        TR(9, ti, 11);
                         if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
-                        TR(1, ti, 12);
+                        TR(9, ti, 12);
                         tc_fence_after();
                         const uint32_t sA = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
 #pragma unroll
@@ -178,9 +178,9 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     for (int i = 0; i < 4; ++i, ++n) {
                         const int slot = n % kRing;
                         mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TR(1, ti, 13);
+                        TR(9, ti, 13);
                         mbar_wait(&p_full[i], u & 1);
-                        TR(1, ti, 14);
+                        TR(9, ti, 14);
                         if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
                         tc_fence_after();
                         const uint32_t sY = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
@@ -216,9 +216,9 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 const int cb = quad * 2 + (u & 1);
                 const uint32_t cbuf = smem_u32(smem + ColSmem::kC + cb * 512);
                 mbar_wait(&c_full[cb], (u >> 1) & 1);
-                if (lane == 0) TR(warp, ti, 21);
+                if (lane == 0) TR(warp + 8, ti, 21);
                 mbar_wait(&s_full[quad], u & 1);
-                if (lane == 0) TR(warp, ti, 22);
+                if (lane == 0) TR(warp + 8, ti, 22);
                 tc_fence_after();
                 float x[kKC];
                 tmem_ld32(tmem + quad * kKC + lane_off, x);
@@ -292,7 +292,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                                  pk[34 + 4 * cc], pk[35 + 4 * cc]);
                 fence_proxy_async_smem();
                 mbar_arrive(&p_full[quad]);
-                if (lane == 0) TR(warp, ti, 23);
+                if (lane == 0) TR(warp + 8, ti, 23);
             }
             // ---- output of the 4 columns: O[l, v] = O^T_i[v, l] / s_l ----
             // tile rows are contiguous W-token grid rows: token(l, j) = row_base(a,0) + j + l*W
@@ -305,10 +305,10 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             const int64_t tok0 = row_base(g, true, a, 0) + j0;
             const int64_t lstep = (int64_t)g.W * g.os[2];
             const int ulast = gi * nch + nch - 1;
-            if (lane == 0) TR(warp, ti, 25);
+            if (lane == 0) TR(warp + 8, ti, 25);
             for (int i = 0; i < 4; ++i) {
                 mbar_wait(&o_done[i], ulast & 1);
-                if (lane == 0) TR(warp, ti, 26);
+                if (lane == 0) TR(warp + 8, ti, 26);
                 tc_fence_after();
                 float o[32];
                 tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
@@ -326,7 +326,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 }
             }
             tc_fence_before();
-            if (lane == 0) TR(warp, ti, 27);
+            if (lane == 0) TR(warp + 8, ti, 27);
             mbar_arrive(o_free);
             named_sync(1, 128);   // stat_sum / rb reused by the next group
         }

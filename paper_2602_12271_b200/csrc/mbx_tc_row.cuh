@@ -18,7 +18,7 @@ struct RowSmem {
     static constexpr int kKV = 2 * kQBytes;           // KV[2]: [K c0 | K c1 | V c0 | V c1] 8 KB each (32 KB)
     static constexpr int kKVBytes = 32768;
     static constexpr int kP = kKV + 2 * kKVBytes;     // P: [128][64] bf16 (16 KB)
-    static constexpr int kStage = kP + 16384;         // epilogue staging [2] x [128][64] bf16 (16 KB each)
+    static constexpr int kStage = kP + 16384;         // epilogue staging [4 warps][2] x [32][64] bf16 (4 KB each)
     static constexpr int kStats = kStage + 2 * 16384; // stats[2][128] float2 (inv_l, c_L)
     static constexpr int kBars = kStats + 2 * 128 * 8;
     static constexpr int kNumBars = 16;
@@ -66,7 +66,8 @@ __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_g
 
 __global__ void __launch_bounds__(kRowThreads, 1)
 tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_wst, Geometry g,
+             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_wst,
+             const __grid_constant__ CUtensorMap tm_wst_b, Geometry g,
              float* __restrict__ Wc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -96,6 +97,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_wst);
+        tma_prefetch(&tm_wst_b);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&q_full[i], 1);
             mbar_init(&q_empty[i], 1);
@@ -269,7 +271,6 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        const bool leader = (warp == 6 && lane == 0);
         int nstore = 0;   // staging buffer uses
         int ti = 0;
         for (int t = 0; t < my_tasks; ++t) {
@@ -283,6 +284,11 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             if (lane == 0 && warp < 8) TR(warp, ti, 31);
             tc_fence_after();
             const float2 st = stats[bsel * 128 + r];
+            // per-warp staging (32 rows x 64 features) and per-warp TMA store: no cross-warp sync
+            const int half = quad & 1;
+            const int nrows = min(32, g.s2 - half * 32);
+            const bool store_ok = a < g.gq && nrows > 0;
+            const int col0 = (bh * g.gq + (a < g.gq ? a : 0)) * g.s2 + half * 32;
             for (int part = 0; part < 4; ++part, ++nstore) {
                 const int sb = nstore & 1;
                 float o[64];
@@ -292,33 +298,28 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                     tc_fence_before();
                     mbar_arrive(&t_empty[bsel]);
                 }
-                // staging buffer sb must have been read by its previous TMA store
-                if (leader) bulk_wait_read<1>();
-                named_sync(2, 128);
-                const uint32_t srow = smem_u32(smem + RowSmem::kStage + sb * 16384) + r * 128;
+                uint8_t* stg = smem + RowSmem::kStage + quad * 8192 + sb * 4096;
+                if (lane == 0) bulk_wait_read<1>();   // previous store from this buffer has read it
+                __syncwarp();
+                const uint32_t srow = smem_u32(stg) + lane * 128;
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc)
-                    st_shared_v4(srow + ((cc ^ (r & 7)) << 4),
+                    st_shared_v4(srow + ((cc ^ (lane & 7)) << 4),
                                  pack_bf16(o[8 * cc] * st.x, o[8 * cc + 1] * st.x),
                                  pack_bf16(o[8 * cc + 2] * st.x, o[8 * cc + 3] * st.x),
                                  pack_bf16(o[8 * cc + 4] * st.x, o[8 * cc + 5] * st.x),
                                  pack_bf16(o[8 * cc + 6] * st.x, o[8 * cc + 7] * st.x));
                 fence_proxy_async_smem();
-                named_sync(2, 128);
-                if (leader) {
-                    for (int qa = 0; qa < 2; ++qa) {
-                        const int aa = tk.mt * 2 + qa;
-                        if (aa >= g.gq) break;
-                        tma_store_4d(&tm_wst, smem + RowSmem::kStage + sb * 16384 + qa * 8192, 0, key, part,
-                                     (bh * g.gq + aa) * g.s2);
-                    }
+                __syncwarp();
+                if (lane == 0 && store_ok) {
+                    tma_store_4d(half ? &tm_wst_b : &tm_wst, stg, 0, key, part, col0);
                     bulk_commit();
                 }
             }
             if (row_ok) Wc[(((int64_t)bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = st.y;
             if (lane == 0 && warp < 8) TR(warp, ti, 32);
         }
-        if (leader) bulk_wait<0>();
+        if (lane == 0) bulk_wait<0>();
     }
     tc_fence_before();
     __syncthreads();

@@ -20,16 +20,16 @@ k = torch.randn(wl["B"], wl["H"], wl["nk"], wl["d"], device=dev, dtype=torch.bfl
 v = torch.randn(wl["B"], wl["H"], wl["nk"], wl["dv"], device=dev, dtype=torch.bfloat16)
 lib = _lib.load()
 lib.mbx_trace_dump.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-buf = np.zeros(4 * 8 * 4096, dtype=np.uint64)
+buf = np.zeros(4 * 16 * 2048, dtype=np.uint64)
 for it in range(3):
     ops.forward(q, k, v, wl["low"], 1)
     torch.cuda.synchronize()
     lib.mbx_trace_dump(buf.ctypes.data, buf.nbytes)   # keep only the last run's trace
-ev = buf.reshape(4, 8, 4096)
+ev = buf.reshape(4, 16, 2048)
 for cta in range(int(os.environ.get("NCTA", "1"))):
     allt = [int(x) >> 8 for x in ev[cta].ravel() if x]
     t0 = min(allt) if allt else 0
-    for role in range(8):
+    for role in range(16):
         xs = [(int(x) >> 8, int(x) & 255) for x in ev[cta, role] if x]
         if not xs:
             continue
