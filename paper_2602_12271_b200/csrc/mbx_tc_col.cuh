@@ -224,18 +224,22 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 tmem_ld32(tmem + quad * kKC + lane_off, x);
                 tmem_ld32(tmem + quad * kKC + 32 + lane_off, x + 32);
                 tmem_ld32(tmem + quad * kKC + 64 + lane_off, x + 64);
-                float mx = -INFINITY;
+                float mq[4] = {-1e30f, -1e30f, -1e30f, -1e30f};
 #pragma unroll
                 for (int k4 = 0; k4 < kKC; k4 += 4) {
                     const float4 c4 = ld_shared_v4f(cbuf + k4 * 4);
-                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int k = k4 + e;
-                        x[k] = k < kvalid ? fmaf(x[k], sl2, -cv[e] * kLog2e) : -INFINITY;
-                        mx = fmaxf(mx, x[k]);
-                    }
+                    x[k4] = fmaf(x[k4], sl2, -c4.x * kLog2e);
+                    x[k4 + 1] = fmaf(x[k4 + 1], sl2, -c4.y * kLog2e);
+                    x[k4 + 2] = fmaf(x[k4 + 2], sl2, -c4.z * kLog2e);
+                    x[k4 + 3] = fmaf(x[k4 + 3], sl2, -c4.w * kLog2e);
                 }
+                if (kvalid < kKC) {   // padded keys -> -1e30 (exp2 -> 0)
+#pragma unroll
+                    for (int k = 0; k < kKC; ++k) x[k] = k < kvalid ? x[k] : -1e30f;
+                }
+#pragma unroll
+                for (int k = 0; k < kKC; ++k) mq[k & 3] = fmaxf(mq[k & 3], x[k]);
+                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
                 tc_fence_before();
                 mbar_arrive(&s_free[quad]);
                 mbar_arrive(&c_empty[cb]);
@@ -245,7 +249,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 if (ch == 0) {
                     m_run = mx;
                 } else if (mx > m_run + 8.f) {
-                    fac = exp2f(m_run - mx);
+                    fac = ex2(m_run - mx);
                     m_run = mx;
                     need = 1;
                 }
@@ -273,13 +277,14 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 }
                 // P_i row l (bf16, K-major SW128: keys 0-63 chunk 0, keys 64-95 chunk 1)
                 uint32_t pk[kKC / 2];
-                float sum = 0.f;
+                float sq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int k = 0; k < kKC; k += 2) {
-                    const float p0 = exp2f(x[k] - m_run), p1 = exp2f(x[k + 1] - m_run);
-                    sum += p0 + p1;
+                    const float p0 = ex2(x[k] - m_run), p1 = ex2(x[k + 1] - m_run);
+                    sq[(k >> 1) & 3] += p0 + p1;
                     pk[k >> 1] = pack_bf16(p0, p1);
                 }
+                const float sum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
                 s_run += sum;
                 if (u > 0) mbar_wait(&o_done[quad], (u - 1) & 1);   // MMA_O_i(u-1) done with P_i
 #pragma unroll

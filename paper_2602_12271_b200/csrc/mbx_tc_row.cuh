@@ -236,23 +236,27 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             float z[64];
             tmem_ld32(tmem + bsel * 256 + lane_off, z);
             tmem_ld32(tmem + bsel * 256 + lane_off + 32, z + 32);
-            float m = -INFINITY;
+            // padded keys -> -1e30 (finite: exp2 -> 0 and 0 * z stays 0)
+            if (g.s2 < 64) {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-                if (i < g.s2) m = fmaxf(m, z[i]);
+                for (int i = 0; i < 64; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+            }
+            float mq[4] = {-1e30f, -1e30f, -1e30f, -1e30f};
+#pragma unroll
+            for (int i = 0; i < 64; ++i) mq[i & 3] = fmaxf(mq[i & 3], z[i]);
+            const float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
             const float mb = m * sl2;
-            float l = 0.f, A = 0.f;
+            float lq[4] = {0.f, 0.f, 0.f, 0.f}, aq[4] = {0.f, 0.f, 0.f, 0.f};
             uint32_t packed[32];
 #pragma unroll
             for (int i = 0; i < 64; i += 2) {
-                float p0 = (i < g.s2) ? exp2f(fmaf(z[i], sl2, -mb)) : 0.f;
-                float p1 = (i + 1 < g.s2) ? exp2f(fmaf(z[i + 1], sl2, -mb)) : 0.f;
-                l += p0 + p1;
-                A = fmaf(p0, (i < g.s2 ? z[i] : 0.f), A);
-                A = fmaf(p1, (i + 1 < g.s2 ? z[i + 1] : 0.f), A);
-                if (!row_ok) p0 = p1 = 0.f;
-                packed[i >> 1] = pack_bf16(p0, p1);
+                const float p0 = ex2(fmaf(z[i], sl2, -mb)), p1 = ex2(fmaf(z[i + 1], sl2, -mb));
+                lq[(i >> 1) & 3] += p0 + p1;
+                aq[(i >> 1) & 3] = fmaf(p1, z[i + 1], fmaf(p0, z[i], aq[(i >> 1) & 3]));
+                packed[i >> 1] = row_ok ? pack_bf16(p0, p1) : 0u;
             }
+            const float l = (lq[0] + lq[1]) + (lq[2] + lq[3]);
+            const float A = (aq[0] + aq[1]) + (aq[2] + aq[3]);
             const float inv_l = 1.f / l;
             // c_L = sum R z - lse with z = scale * S
             stats[bsel * 128 + r] = make_float2(inv_l, g.scale * (A * inv_l - m) - __logf(l));
