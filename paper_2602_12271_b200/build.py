@@ -47,7 +47,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     tmp = os.path.join(HERE, "_build")
     os.makedirs(tmp, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                    "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+                    "--expt-relaxed-constexpr", "-diag-suppress", "177", "-I", os.path.join(ROOT, "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
     if trace:

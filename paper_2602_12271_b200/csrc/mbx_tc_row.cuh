@@ -167,10 +167,9 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const uint32_t p_base = smem_u32(smem + RowSmem::kP);
             uint32_t nq = 0, nkv = 0;
             int ti = 0;
-            auto issue_s = [&](int t, const RowTask& tk) {   // MMA1 for task t
+            auto issue_s = [&](int t, const RowTask& tk) {   // MMA1 for task t (TMEM buffer t%2 free)
                 const int qs = (nq - 1) & 1, ks = (nkv - 1) & 1;
                 const int bsel = t & 1;
-                mbar_wait(&t_empty[bsel], ring_parity(t, 2) ^ 1);
                 TR(1, ti, 11);
                 tc_fence_after();
                 const uint32_t qbase = smem_u32(smem + RowSmem::kQ + qs * RowSmem::kQBytes);
@@ -183,38 +182,56 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 }
                 mma_commit(&s_full[bsel]);
             };
+            auto acquire = [&](const RowTask& tk) {   // operands of a task about to get its MMA1
+                if (tk.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; }
+                if (tk.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; }
+            };
+            if (my_tasks > 0) {
+                const RowTask t0 = row_task(0, n_mt, g.gk, first_item, item_stride);
+                acquire(t0);
+                issue_s(0, t0);
+            }
             for (int t = 0; t < my_tasks; ++t) {
                 const RowTask cur = row_task(t, n_mt, g.gk, first_item, item_stride);
-                if (t == 0) {
-                    if (cur.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; }
-                    if (cur.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; }
-                    issue_s(t, cur);
-                }
-                // look ahead: MMA1(t+1) before MMA2(t) so it overlaps softmax(t)
+                // MMA1(t+1) and MMA2(t) are independent: issue whichever is ready first
+                // (MMA1(t+1) waits for the epilogue of t-1 to free TMEM buffer (t+1)%2,
+                // MMA2(t) for softmax(t)), so neither chain stalls the other.
+                const bool has_next = t + 1 < my_tasks;
+                const RowTask nx = row_task(has_next ? t + 1 : t, n_mt, g.gk, first_item, item_stride);
+                bool s_done = !has_next, o_done = false;
                 int adv = 0, advq = 0;
-                if (t + 1 < my_tasks) {
-                    const RowTask nx = row_task(t + 1, n_mt, g.gk, first_item, item_stride);
-                    if (nx.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; advq = 1; }
-                    if (nx.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; adv = 1; }
+                while (!o_done) {
+                    if (!s_done && mbar_test(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1)) {
+                        advq = nx.first_of_item;
+                        adv = nx.first_of_c;
+                        acquire(nx);
+                        issue_s(t + 1, nx);
+                        s_done = true;
+                    }
+                    if (mbar_test(p_full, ring_parity(t, 1))) {
+                        // MMA2(t): [aL | Y] = P . [K | V]
+                        TR(1, ti, 12);
+                        tc_fence_after();
+                        const int ks = (nkv - 1 - adv) & 1;
+                        const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t ad = smem_desc(p_base + kk * 32, 16, 1024, 2);
+                            const uint64_t bd = smem_desc(kbase + kk * 2048, 8192, 1024, 2);
+                            mma_bf16(tmem + (t & 1) * 256, ad, bd, idesc_o, kk > 0);
+                        }
+                        mma_commit(&o_full[t & 1]);
+                        mma_commit(p_empty);
+                        if (cur.last_of_c) mma_commit(&kv_empty[ks]);
+                        if (cur.last_of_item) mma_commit(&q_empty[(nq - 1 - advq) & 1]);
+                        o_done = true;
+                    }
+                }
+                if (!s_done) {
+                    mbar_wait(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1);
+                    acquire(nx);
                     issue_s(t + 1, nx);
                 }
-                // MMA2(t): [aL | Y] = P . [K | V]
-                const int bsel = t & 1;
-                mbar_wait(p_full, ring_parity(t, 1));
-                TR(1, ti, 12);
-                tc_fence_after();
-                const int ks = (nkv - 1 - adv) & 1;
-                const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    const uint64_t ad = smem_desc(p_base + kk * 32, 16, 1024, 2);
-                    const uint64_t bd = smem_desc(kbase + kk * 2048, 8192, 1024, 2);
-                    mma_bf16(tmem + bsel * 256, ad, bd, idesc_o, kk > 0);
-                }
-                mma_commit(&o_full[bsel]);
-                mma_commit(p_empty);
-                if (cur.last_of_c) mma_commit(&kv_empty[ks]);
-                if (cur.last_of_item) mma_commit(&q_empty[(nq - 1 - advq) & 1]);
             }
         }
     } else if (warp < 6) {
@@ -253,11 +270,16 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 const float p0 = ex2(fmaf(z[i], sl2, -mb)), p1 = ex2(fmaf(z[i + 1], sl2, -mb));
                 lq[(i >> 1) & 3] += p0 + p1;
                 aq[(i >> 1) & 3] = fmaf(p1, z[i + 1], fmaf(p0, z[i], aq[(i >> 1) & 3]));
-                packed[i >> 1] = row_ok ? pack_bf16(p0, p1) : 0u;
+                z[i] = p0;
+                z[i + 1] = p1;
             }
             const float l = (lq[0] + lq[1]) + (lq[2] + lq[3]);
             const float A = (aq[0] + aq[1]) + (aq[2] + aq[3]);
             const float inv_l = 1.f / l;
+            // R = p / l goes into P (bf16, <= 1), so MMA2 yields normalised aL and Y
+            const float pscale = row_ok ? inv_l : 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(z[i] * pscale, z[i + 1] * pscale);
             // c_L = sum R z - lse with z = scale * S
             stats[bsel * 128 + r] = make_float2(inv_l, g.scale * (A * inv_l - m) - __logf(l));
             tc_fence_before();
@@ -309,10 +331,8 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc)
                     st_shared_v4(srow + ((cc ^ (lane & 7)) << 4),
-                                 pack_bf16(o[8 * cc] * st.x, o[8 * cc + 1] * st.x),
-                                 pack_bf16(o[8 * cc + 2] * st.x, o[8 * cc + 3] * st.x),
-                                 pack_bf16(o[8 * cc + 4] * st.x, o[8 * cc + 5] * st.x),
-                                 pack_bf16(o[8 * cc + 6] * st.x, o[8 * cc + 7] * st.x));
+                                 pack_bf16(o[8 * cc], o[8 * cc + 1]), pack_bf16(o[8 * cc + 2], o[8 * cc + 3]),
+                                 pack_bf16(o[8 * cc + 4], o[8 * cc + 5]), pack_bf16(o[8 * cc + 6], o[8 * cc + 7]));
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0 && store_ok) {
