@@ -84,6 +84,14 @@ bool make_rows_map(CUtensorMap* m, const void* base, int B, int H, int N, const 
 }
 
 // Query columns: q viewed as (d, w-column, grid row of W tokens, b*H+h); box (64, 1, 32, 1).
+// Output columns: out viewed like q; box (32 value dims, 1, s1 rows, 1), no swizzle.
+bool make_outcol_map(CUtensorMap* m, const void* base, const Geometry& g, int nq) {
+    cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
+    cuuint64_t strides[3] = {(cuuint64_t)g.os[2] * 2, (cuuint64_t)g.os[2] * 2 * g.W, (cuuint64_t)g.os[1] * 2};
+    cuuint32_t box[4] = {32, 1, (cuuint32_t)g.s1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
 bool make_qcol_map(CUtensorMap* m, const void* base, const Geometry& g, int nq) {
     cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
     cuuint64_t strides[3] = {(cuuint64_t)g.qs[2] * 2, (cuuint64_t)g.qs[2] * 2 * g.W, (cuuint64_t)g.qs[1] * 2};
@@ -133,6 +141,7 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
     if (!column_grid(g, &F, &H, &W)) return false;
     if (!strides_ok(g.qs) || !strides_ok(g.ks) || !strides_ok(g.vs) || !strides_ok(g.os)) return false;
     if (g.bh > 1 && g.qs[0] != (int64_t)g.heads * g.qs[1]) return false;   // qcol map folds (b, h)
+    if (g.bh > 1 && g.os[0] != (int64_t)g.heads * g.os[1]) return false;   // output map folds (b, h)
     if ((int64_t)g.bh * g.gq * g.s2 * g.nkeys >= ((int64_t)1 << 31)) return false;
     return encode_fn() != nullptr;
 }
@@ -155,9 +164,10 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
         return cudaErrorInvalidValue;
-    CUtensorMap tq, tk, tv, tqc, tw, tws, tws_b, tc;
+    CUtensorMap tq, tk, tv, tqc, tw, tws, tws_b, tc, tout;
     if (!make_rows_map(&tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&tk, k, B, g.heads, nk, g.ks, g.s2) ||
-        !make_rows_map(&tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&tqc, q, g, nq))
+        !make_rows_map(&tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&tqc, q, g, nq) ||
+        !make_outcol_map(&tout, out, g, nq))
         return cudaErrorInvalidValue;
     const int64_t ncols = (int64_t)g.bh * g.gq * g.s2;
     const int64_t rows = ncols * g.nkeys;
@@ -202,8 +212,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int grid_col = ngroups < num_sms() ? (int)ngroups : num_sms();
     {
         ProfScope p("tc_column_stage", stream);
-        tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(tw, tc, tqc, g,
-                                                                      reinterpret_cast<__nv_bfloat16*>(out));
+        tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(tw, tc, tqc, tout, g);
     }
     return cudaGetLastError();
 }

@@ -14,14 +14,15 @@
 // (solver.py:192-195 joint softmax with bias -c_L; factors.py:124 O = L Y).
 constexpr int kColThreads = 192;   // 6 warps: producer, MMA, 4 x softmax/output
 constexpr int kKC = 96;            // keys per chunk (S_i is 96 TMEM columns)
-constexpr int kRing = 6;           // aL / Y chunk slots
+constexpr int kRing = 5;           // aL / Y chunk slots
 struct ColSmem {
     static constexpr int kQ = 0;                          // Qstack: 2 d-chunks x [128][64] (32 KB)
     static constexpr int kSlot = 2 * kKC * 128;           // [96 keys][128 feat] as 2 x [96][64] (24 KB)
     static constexpr int kRingOff = 32768;
     static constexpr int kP = kRingOff + kRing * kSlot;   // P_i: 2 x [32 l][64 keys] (8 KB each)
     static constexpr int kC = kP + 4 * 8192;              // c_L chunks: [4 columns][2 buffers] x 96 floats (512 B pitch)
-    static constexpr int kStat = kC + 8 * 512;            // row sums [4][32], rescale [4][32], flags [4], rb[32]
+    static constexpr int kOut = kC + 8 * 512;             // output staging [4 warps][4 columns] x [32 rows][64 B]
+    static constexpr int kStat = kOut + 16 * 2048;        // row sums [4][32], rescale [4][32], flags [4], rb[32]
     static constexpr int kBars = kStat + 4 * 32 * 4 * 2 + 4 * 4 + 32 * 8;
     static constexpr int kNumBars = 2 * kRing + 2 + 4 * 4 + 1 + 16;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
@@ -30,7 +31,7 @@ struct ColSmem {
 
 __global__ void __launch_bounds__(kColThreads, 1)
 tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_c,
-                const __grid_constant__ CUtensorMap tm_qc, Geometry g, __nv_bfloat16* __restrict__ out) {
+                const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_out, Geometry g) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ColSmem::kBars);
@@ -62,6 +63,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
         tma_prefetch(&tm_w);
         tma_prefetch(&tm_c);
         tma_prefetch(&tm_qc);
+        tma_prefetch(&tm_out);
         for (int i = 0; i < kRing; ++i) {
             mbar_init(&ring_full[i], 1);
             mbar_init(&ring_empty[i], 1);
@@ -306,9 +308,14 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             named_sync(1, 128);
             const int v = quad * 32 + lane;              // this thread's TMEM lane = value dim
             const int b = bh / g.heads, h = bh % g.heads;
-            __nv_bfloat16* ob = out + b * g.os[0] + h * g.os[1] + v;
+            (void)b;
+            (void)h;
+            (void)v;
             const int64_t tok0 = row_base(g, true, a, 0) + j0;
-            const int64_t lstep = (int64_t)g.W * g.os[2];
+            // this warp's output staging (its 32 value dims of each row l) must have been read
+            // by the previous group's TMA stores before it is rewritten
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
             const int ulast = gi * nch + nch - 1;
             if (lane == 0) TR(warp + 8, ti, 25);
             for (int i = 0; i < 4; ++i) {
@@ -317,6 +324,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 tc_fence_after();
                 float o[32];
                 tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
+                if (lane == 0) TR(warp + 8, ti, 28);
                 float inv[32];
 #pragma unroll
                 for (int q4 = 0; q4 < 32; q4 += 4) {
@@ -324,11 +332,25 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     inv[q4] = t4.x; inv[q4 + 1] = t4.y; inv[q4 + 2] = t4.z; inv[q4 + 3] = t4.w;
                 }
                 if (j0 + i < g.s2) {
-                    __nv_bfloat16* col = ob + (tok0 + i) * g.os[2];
+                    // rows l of column j: smem [l][64 B] (this warp's value dims), one TMA store
+                    const uint32_t stg = smem_u32(smem + ColSmem::kOut + (quad * 4 + i) * 2048) + lane * 2;
 #pragma unroll
-                    for (int q = 0; q < 32; ++q)
-                        if (q < g.s1) col[q * lstep] = __float2bfloat16_rn(o[q] * inv[q]);
+                    for (int q = 0; q < 32; ++q) {
+                        const __nv_bfloat16 hv = __float2bfloat16_rn(o[q] * inv[q]);
+                        asm volatile("st.shared.b16 [%0], %1;" ::"r"(stg + q * 64),
+                                     "h"(*reinterpret_cast<const unsigned short*>(&hv))
+                                     : "memory");
+                    }
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int64_t tok = tok0 + i;
+                        tma_store_4d(&tm_out, smem + ColSmem::kOut + (quad * 4 + i) * 2048, quad * 32,
+                                     (int)(tok % g.W), (int)(tok / g.W), bh);
+                        bulk_commit();
+                    }
                 }
+                if (lane == 0) TR(warp + 8, ti, 29);
             }
             tc_fence_before();
             if (lane == 0) TR(warp + 8, ti, 27);
@@ -336,6 +358,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
             named_sync(1, 128);   // stat_sum / rb reused by the next group
         }
     }
+    if (warp >= 2 && lane == 0) bulk_wait<0>();
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc<512>(tmem);
