@@ -324,6 +324,9 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                     tc_fence_before();
                     mbar_arrive(&t_empty[bsel]);
                 }
+                // a warp whose rows are all padding (a >= G_q) writes nothing: touching the
+                // staging buffer would race with this warp's in-flight TMA store from it
+                if (!store_ok) continue;
                 uint8_t* stg = smem + RowSmem::kStage + quad * 8192 + sb * 4096;
                 if (lane == 0) bulk_wait_read<1>();   // previous store from this buffer has read it
                 __syncwarp();
@@ -335,7 +338,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                                  pack_bf16(o[8 * cc + 4], o[8 * cc + 5]), pack_bf16(o[8 * cc + 6], o[8 * cc + 7]));
                 fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0 && store_ok) {
+                if (lane == 0) {
                     tma_store_4d(half ? &tm_wst_b : &tm_wst, stg, 0, key, part, col0);
                     bulk_commit();
                 }

@@ -155,12 +155,14 @@ def test_strided_batch_heads_and_permuted_plan(cuda):
 
 
 def test_deterministic_bitwise(cuda):
+    """Back-to-back launches (no host sync, fresh workspaces from the caching
+    allocator) must agree bitwise: catches races between pipeline stages."""
     g = torch.Generator(device="cpu").manual_seed(4)
-    q, k, v = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    q, k, v = (torch.randn(1, 12, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
     plan = _sf_plan()
-    a = pk.monarch_attention(q, k, v, plan)
-    b = pk.monarch_attention(q, k, v, plan)
-    assert torch.equal(a, b)
+    outs = [pk.monarch_attention(q, k, v, plan) for _ in range(16)]
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
 
 
 def test_factors_row_stochastic_on_device(cuda):
