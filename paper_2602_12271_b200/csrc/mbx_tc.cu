@@ -202,7 +202,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     if ((e = cudaFuncSetAttribute(tc_column_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_col)) !=
         cudaSuccess)
         return e;
-    const int items = g.bh * g.s1;
+    const int items = g.bh * g.s1 * ((g.gq + 1) / 2);   // row-stage items (b, h, k, M tile)
     const int grid_row = items < num_sms() ? items : num_sms();
     {
         ProfScope p("tc_row_stage", stream);

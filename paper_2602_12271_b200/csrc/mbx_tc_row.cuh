@@ -1,54 +1,47 @@
 // Row stage (included by mbx_tc.cu).
 //
-// Item = (b, h, in-tile row k): the Q rows k of all query tiles stay in smem
-// while the K/V rows k of every key tile c stream through a 2-stage TMA ring.
-// Per task (c, M-tile of two query tiles):
+// Item = (b, h, in-tile row k, M-tile mt): the Q rows k of query tiles
+// 2mt, 2mt+1 (one 128-row M tile) stay in smem while the K/V rows k of every
+// key tile c stream through a 2-stage TMA ring.  Per task (key tile c):
 //   MMA1  S[(a,j), i] = Q_k . K_ck^T        128 x 64 x 128      -> TMEM buffer t%2
-//   softmax_i (warps 2-5, one query row per thread), c_L = sum R z - lse
+//   softmax_i (warps 2-5, one query row per thread), c_L = sum R z - lse,
+//   R = p / l written as bf16 P (double-buffered)
 //   MMA2  [aL | Y]    = P . [K_ck | V_ck]   128 x 256 x 64      -> same TMEM buffer
-//   epilogue (warps 6-9): * 1/l, bf16, staged in smem, TMA-stored to the blocked
-//   workspace W[col][part][key][64] (part 0,1 = aL halves, 2,3 = Y halves), so the
-//   column stage reads contiguous 12 KB boxes.  (solver.py:187-191, factors.py:123)
+//   epilogue (warps 6-9): TMEM -> bf16 -> per-warp smem staging -> TMA store into the
+//   blocked workspace W[col][part][key][64] (part 0,1 = aL halves, 2,3 = Y halves),
+//   so the column stage reads contiguous 12 KB boxes.
+// (solver.py:187-191 R update and c_L; factors.py:123 Y = R V; tensorops.py:268-272)
 constexpr int kRowThreads = 320;   // 10 warps
 struct RowSmem {
-    // Q[2] (48 KB each): query tile a < 2 -> d-chunk c at c*16K + a*8K (M tile 0 rows a*64..);
-    // a == 2 -> M tile 1 at 32K + c*8K (its rows 64..127 read the next 8 KB: discarded rows).
+    // Q[2] (32 KB each): d-chunk c at c*16K, query tile 2mt+la at rows la*64.. (+la*8K)
     static constexpr int kQ = 0;
-    static constexpr int kQBytes = 49152;
+    static constexpr int kQBytes = 32768;
     static constexpr int kKV = 2 * kQBytes;           // KV[2]: [K c0 | K c1 | V c0 | V c1] 8 KB each (32 KB)
     static constexpr int kKVBytes = 32768;
-    static constexpr int kP = kKV + 2 * kKVBytes;     // P: [128][64] bf16 (16 KB)
-    static constexpr int kStage = kP + 16384;         // epilogue staging [4 warps][2] x [32][64] bf16 (4 KB each)
-    static constexpr int kStats = kStage + 2 * 16384; // stats[2][128] float2 (inv_l, c_L)
-    static constexpr int kBars = kStats + 2 * 128 * 8;
-    static constexpr int kNumBars = 16;
+    static constexpr int kP = kKV + 2 * kKVBytes;     // P[2]: [128][64] bf16 (16 KB each)
+    static constexpr int kStage = kP + 2 * 16384;     // epilogue staging [4 warps][2] x [32][64] bf16 (4 KB each)
+    static constexpr int kStats = kStage + 2 * 16384; // c_L[2][128] floats
+    static constexpr int kBars = kStats + 2 * 128 * 4;
+    static constexpr int kNumBars = 18;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
 
-__host__ __device__ __forceinline__ int q_slot_off(int a, int c) {
-    return a < 2 ? c * 16384 + a * 8192 : 32768 + c * 8192;
-}
-__host__ __device__ __forceinline__ int q_tile_off(int mt, int c) {
-    return mt == 0 ? c * 16384 : 32768 + c * 8192;
-}
-
-struct RowTask {            // decoded task t of this CTA
-    int item, c, mt;
-    bool first_of_item, last_of_item, first_of_c, last_of_c;
+struct RowTask {            // decoded task t of this CTA: item (b,h,k,mt), key tile c
+    int bh, kr, mt, c;
+    bool first_of_item, last_of_item;
 };
 
-__device__ __forceinline__ RowTask row_task(int t, int n_mt, int gk, int first_item, int item_stride) {
+__device__ __forceinline__ RowTask row_task(const Geometry& g, int t, int n_mt, int first_item, int item_stride) {
     RowTask r;
-    const int per_item = n_mt * gk;
-    const int li = t / per_item, rem = t - li * per_item;
-    r.item = first_item + li * item_stride;
-    r.c = rem / n_mt;
-    r.mt = rem - r.c * n_mt;
-    r.first_of_item = rem == 0;
-    r.last_of_item = rem == per_item - 1;
-    r.first_of_c = r.mt == 0;
-    r.last_of_c = r.mt == n_mt - 1;
+    const int li = t / g.gk;
+    r.c = t - li * g.gk;
+    const int item = first_item + li * item_stride;   // item = (bh * s1 + k) * n_mt + mt
+    r.mt = item % n_mt;
+    r.kr = (item / n_mt) % g.s1;
+    r.bh = item / (n_mt * g.s1);
+    r.first_of_item = r.c == 0;
+    r.last_of_item = r.c == g.gk - 1;
     return r;
 }
 
@@ -67,8 +60,7 @@ __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_g
 __global__ void __launch_bounds__(kRowThreads, 1)
 tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
              const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_wst,
-             const __grid_constant__ CUtensorMap tm_wst_b, Geometry g,
-             float* __restrict__ Wc) {
+             const __grid_constant__ CUtensorMap tm_wst_b, Geometry g, float* __restrict__ Wc) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RowSmem::kBars);
@@ -79,17 +71,17 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
     uint64_t* s_full = bars + 8;    // [2]
     uint64_t* o_full = bars + 10;   // [2]
     uint64_t* t_empty = bars + 12;  // [2]
-    uint64_t* p_full = bars + 14;   // [1]
-    uint64_t* p_empty = bars + 15;  // [1]
-    float2* stats = reinterpret_cast<float2*>(smem + RowSmem::kStats);
+    uint64_t* p_full = bars + 14;   // [2]
+    uint64_t* p_empty = bars + 16;  // [2]
+    float* stats = reinterpret_cast<float*>(smem + RowSmem::kStats);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowSmem::kTmemSlot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    const int items = g.bh * g.s1;
+    const int n_mt = (g.gq + 1) >> 1;
+    const int items = g.bh * g.s1 * n_mt;
     const int first_item = blockIdx.x, item_stride = gridDim.x;
     const int my_items = first_item < items ? (items - first_item + item_stride - 1) / item_stride : 0;
-    const int n_mt = (g.gq + 1) >> 1;
-    const int my_tasks = my_items * g.gk * n_mt;
+    const int my_tasks = my_items * g.gk;
     const uint32_t box_bytes = (uint32_t)g.s2 * 128u;
 
     if (tid == 0) {
@@ -106,13 +98,13 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             mbar_init(&s_full[i], 1);
             mbar_init(&o_full[i], 1);
             mbar_init(&t_empty[i], 128);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&p_empty[i], 1);
         }
-        mbar_init(p_full, 128);
-        mbar_init(p_empty, 1);
         fence_barrier_init();
     }
-    // Rows s2..63 of every box slot are never written by TMA (box = s2 rows): zero
-    // the operand buffers once so MMA padding rows/keys read zeros.
+    // Rows s2..63 of every box slot (and the second query-tile slot of an odd last
+    // M tile) are never written by TMA: zero them once so MMA padding reads zeros.
     for (int i = tid; i < (2 * RowSmem::kQBytes + 2 * RowSmem::kKVBytes) / 16; i += kRowThreads)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -125,38 +117,33 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
-            uint32_t nq = 0, nkv = 0;
             int ti = 0;
             for (int t = 0; t < my_tasks; ++t) {
-                const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
-                const int kr = tk.item % g.s1, bh = tk.item / g.s1;
-                const int b = bh / g.heads, h = bh % g.heads;
+                const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
+                const int b = tk.bh / g.heads, h = tk.bh % g.heads;
                 if (tk.first_of_item) {
-                    const int qs = nq & 1;
-                    mbar_wait(&q_empty[qs], ring_parity(nq, 2) ^ 1);
+                    const int li = t / g.gk, qs = li & 1;
+                    mbar_wait(&q_empty[qs], ring_parity(li, 2) ^ 1);
                     TR(0, ti, 1);
-                    mbar_expect_tx(&q_full[qs], 2u * box_bytes * (uint32_t)g.gq);
+                    const int nqa = min(2, g.gq - 2 * tk.mt);
+                    mbar_expect_tx(&q_full[qs], 2u * box_bytes * (uint32_t)nqa);
                     uint8_t* qb = smem + RowSmem::kQ + qs * RowSmem::kQBytes;
-                    for (int a = 0; a < g.gq; ++a) {
-                        const int tok = (int)row_base(g, true, a, kr);
-                        tma_load_4d(qb + q_slot_off(a, 0), &tm_q, &q_full[qs], 0, tok, h, b);
-                        tma_load_4d(qb + q_slot_off(a, 1), &tm_q, &q_full[qs], 64, tok, h, b);
+                    for (int la = 0; la < nqa; ++la) {
+                        const int tok = (int)row_base(g, true, 2 * tk.mt + la, tk.kr);
+                        tma_load_4d(qb + la * 8192, &tm_q, &q_full[qs], 0, tok, h, b);
+                        tma_load_4d(qb + 16384 + la * 8192, &tm_q, &q_full[qs], 64, tok, h, b);
                     }
-                    ++nq;
                 }
-                if (tk.first_of_c) {
-                    const int ks = nkv & 1;
-                    mbar_wait(&kv_empty[ks], ring_parity(nkv, 2) ^ 1);
-                    TR(0, ti, 2);
-                    mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
-                    uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
-                    const int tok = (int)row_base(g, false, tk.c, kr);
-                    tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
-                    tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
-                    tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
-                    tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
-                    ++nkv;
-                }
+                const int ks = t & 1;
+                mbar_wait(&kv_empty[ks], ring_parity(t, 2) ^ 1);
+                TR(0, ti, 2);
+                mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
+                uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
+                const int tok = (int)row_base(g, false, tk.c, tk.kr);
+                tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
+                tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
+                tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
+                tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
             }
         }
     } else if (warp == 1) {
@@ -164,73 +151,56 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         if (lane == 0) {
             const uint32_t idesc_s = idesc_bf16(128, 64, false, false);
             const uint32_t idesc_o = idesc_bf16(128, 256, false, true);
-            const uint32_t p_base = smem_u32(smem + RowSmem::kP);
-            uint32_t nq = 0, nkv = 0;
             int ti = 0;
-            auto issue_s = [&](int t, const RowTask& tk) {   // MMA1 for task t (TMEM buffer t%2 free)
-                const int qs = (nq - 1) & 1, ks = (nkv - 1) & 1;
-                const int bsel = t & 1;
+            auto issue_s = [&](int t) {   // MMA1(t): TMEM buffer t%2 must be free
+                const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
+                const int li = t / g.gk;
+                if (tk.first_of_item) mbar_wait(&q_full[li & 1], ring_parity(li, 2));
+                mbar_wait(&kv_full[t & 1], ring_parity(t, 2));
                 TR(1, ti, 11);
                 tc_fence_after();
-                const uint32_t qbase = smem_u32(smem + RowSmem::kQ + qs * RowSmem::kQBytes);
-                const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
+                const uint32_t qbase = smem_u32(smem + RowSmem::kQ + (li & 1) * RowSmem::kQBytes);
+                const uint32_t kbase = smem_u32(smem + RowSmem::kKV + (t & 1) * RowSmem::kKVBytes);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = smem_desc(qbase + q_tile_off(tk.mt, kk >> 2) + (kk & 3) * 32, 16, 1024, 2);
+                    const uint64_t ad = smem_desc(qbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
                     const uint64_t bd = smem_desc(kbase + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2);
-                    mma_bf16(tmem + bsel * 256, ad, bd, idesc_s, kk > 0);
+                    mma_bf16(tmem + (t & 1) * 256, ad, bd, idesc_s, kk > 0);
                 }
-                mma_commit(&s_full[bsel]);
+                mma_commit(&s_full[t & 1]);
             };
-            auto acquire = [&](const RowTask& tk) {   // operands of a task about to get its MMA1
-                if (tk.first_of_item) { mbar_wait(&q_full[nq & 1], ring_parity(nq, 2)); ++nq; }
-                if (tk.first_of_c) { mbar_wait(&kv_full[nkv & 1], ring_parity(nkv, 2)); ++nkv; }
-            };
-            if (my_tasks > 0) {
-                const RowTask t0 = row_task(0, n_mt, g.gk, first_item, item_stride);
-                acquire(t0);
-                issue_s(0, t0);
-            }
+            if (my_tasks > 0) issue_s(0);
             for (int t = 0; t < my_tasks; ++t) {
-                const RowTask cur = row_task(t, n_mt, g.gk, first_item, item_stride);
-                // MMA1(t+1) and MMA2(t) are independent: issue whichever is ready first
-                // (MMA1(t+1) waits for the epilogue of t-1 to free TMEM buffer (t+1)%2,
-                // MMA2(t) for softmax(t)), so neither chain stalls the other.
-                const bool has_next = t + 1 < my_tasks;
-                const RowTask nx = row_task(has_next ? t + 1 : t, n_mt, g.gk, first_item, item_stride);
-                bool s_done = !has_next, o_done = false;
-                int adv = 0, advq = 0;
+                const RowTask cur = row_task(g, t, n_mt, first_item, item_stride);
+                // MMA1(t+1) waits for the epilogue of t-1 to free TMEM buffer (t+1)%2, MMA2(t)
+                // for softmax(t): issue whichever is ready first so neither chain stalls the other.
+                bool s_done = t + 1 >= my_tasks, o_done = false;
                 while (!o_done) {
                     if (!s_done && mbar_test(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1)) {
-                        advq = nx.first_of_item;
-                        adv = nx.first_of_c;
-                        acquire(nx);
-                        issue_s(t + 1, nx);
+                        issue_s(t + 1);
                         s_done = true;
                     }
-                    if (mbar_test(p_full, ring_parity(t, 1))) {
-                        // MMA2(t): [aL | Y] = P . [K | V]
+                    if (mbar_test(&p_full[t & 1], ring_parity(t, 2))) {
                         TR(1, ti, 12);
                         tc_fence_after();
-                        const int ks = (nkv - 1 - adv) & 1;
-                        const uint32_t kbase = smem_u32(smem + RowSmem::kKV + ks * RowSmem::kKVBytes);
+                        const uint32_t pbase = smem_u32(smem + RowSmem::kP + (t & 1) * 16384);
+                        const uint32_t kbase = smem_u32(smem + RowSmem::kKV + (t & 1) * RowSmem::kKVBytes);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t ad = smem_desc(p_base + kk * 32, 16, 1024, 2);
+                            const uint64_t ad = smem_desc(pbase + kk * 32, 16, 1024, 2);
                             const uint64_t bd = smem_desc(kbase + kk * 2048, 8192, 1024, 2);
                             mma_bf16(tmem + (t & 1) * 256, ad, bd, idesc_o, kk > 0);
                         }
                         mma_commit(&o_full[t & 1]);
-                        mma_commit(p_empty);
-                        if (cur.last_of_c) mma_commit(&kv_empty[ks]);
-                        if (cur.last_of_item) mma_commit(&q_empty[(nq - 1 - advq) & 1]);
+                        mma_commit(&p_empty[t & 1]);
+                        mma_commit(&kv_empty[t & 1]);
+                        if (cur.last_of_item) mma_commit(&q_empty[(t / g.gk) & 1]);
                         o_done = true;
                     }
                 }
                 if (!s_done) {
                     mbar_wait(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1);
-                    acquire(nx);
-                    issue_s(t + 1, nx);
+                    issue_s(t + 1);
                 }
             }
         }
@@ -239,11 +209,10 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        const uint32_t p_row = smem_u32(smem + RowSmem::kP) + r * 128;
         const float sl2 = g.scale * kLog2e;
         int ti = 0;
         for (int t = 0; t < my_tasks; ++t) {
-            const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
+            const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
             const int bsel = t & 1;
             const int a = tk.mt * 2 + (r >> 6), j = r & 63;
             const bool row_ok = a < g.gq && j < g.s2;
@@ -264,7 +233,6 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
             const float mb = m * sl2;
             float lq[4] = {0.f, 0.f, 0.f, 0.f}, aq[4] = {0.f, 0.f, 0.f, 0.f};
-            uint32_t packed[32];
 #pragma unroll
             for (int i = 0; i < 64; i += 2) {
                 const float p0 = ex2(fmaf(z[i], sl2, -mb)), p1 = ex2(fmaf(z[i + 1], sl2, -mb));
@@ -276,20 +244,22 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
             const float l = (lq[0] + lq[1]) + (lq[2] + lq[3]);
             const float A = (aq[0] + aq[1]) + (aq[2] + aq[3]);
             const float inv_l = 1.f / l;
+            // c_L = sum R z - lse with z = scale * S
+            stats[bsel * 128 + r] = g.scale * (A * inv_l - m) - __logf(l);
             // R = p / l goes into P (bf16, <= 1), so MMA2 yields normalised aL and Y
             const float pscale = row_ok ? inv_l : 0.f;
+            uint32_t packed[32];
 #pragma unroll
             for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(z[i] * pscale, z[i + 1] * pscale);
-            // c_L = sum R z - lse with z = scale * S
-            stats[bsel * 128 + r] = make_float2(inv_l, g.scale * (A * inv_l - m) - __logf(l));
             tc_fence_before();
-            mbar_wait(p_empty, ring_parity(t, 1) ^ 1);
+            mbar_wait(&p_empty[bsel], ring_parity(t, 2) ^ 1);   // MMA2(t-2) done with P[bsel]
+            const uint32_t p_row = smem_u32(smem + RowSmem::kP + bsel * 16384) + r * 128;
 #pragma unroll
             for (int cc = 0; cc < 8; ++cc)
                 st_shared_v4(p_row + ((cc ^ (r & 7)) << 4), packed[4 * cc], packed[4 * cc + 1],
                              packed[4 * cc + 2], packed[4 * cc + 3]);
             fence_proxy_async_smem();
-            mbar_arrive(p_full);
+            mbar_arrive(&p_full[bsel]);
             if (lane == 0) TR(warp, ti, 22);
         }
     } else {
@@ -297,26 +267,24 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        int nstore = 0;   // staging buffer uses
+        int nstore = 0;   // staging buffer uses of this warp
         int ti = 0;
         for (int t = 0; t < my_tasks; ++t) {
-            const RowTask tk = row_task(t, n_mt, g.gk, first_item, item_stride);
+            const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
             const int bsel = t & 1;
             const int a = tk.mt * 2 + (r >> 6), j = r & 63;
             const bool row_ok = a < g.gq && j < g.s2;
-            const int kr = tk.item % g.s1, bh = tk.item / g.s1;
-            const int key = tk.c * g.s1 + kr;
+            const int key = tk.c * g.s1 + tk.kr;
             mbar_wait(&o_full[bsel], ring_parity(t, 2));
             if (lane == 0 && warp < 8) TR(warp, ti, 31);
             tc_fence_after();
-            const float2 st = stats[bsel * 128 + r];
+            const float c_l = stats[bsel * 128 + r];
             // per-warp staging (32 rows x 64 features) and per-warp TMA store: no cross-warp sync
             const int half = quad & 1;
             const int nrows = min(32, g.s2 - half * 32);
             const bool store_ok = a < g.gq && nrows > 0;
-            const int col0 = (bh * g.gq + (a < g.gq ? a : 0)) * g.s2 + half * 32;
-            for (int part = 0; part < 4; ++part, ++nstore) {
-                const int sb = nstore & 1;
+            const int col0 = (tk.bh * g.gq + (a < g.gq ? a : 0)) * g.s2 + half * 32;
+            for (int part = 0; part < 4; ++part) {
                 float o[64];
                 tmem_ld32(tmem + bsel * 256 + lane_off + part * 64, o);
                 tmem_ld32(tmem + bsel * 256 + lane_off + part * 64 + 32, o + 32);
@@ -327,6 +295,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                 // a warp whose rows are all padding (a >= G_q) writes nothing: touching the
                 // staging buffer would race with this warp's in-flight TMA store from it
                 if (!store_ok) continue;
+                const int sb = nstore++ & 1;
                 uint8_t* stg = smem + RowSmem::kStage + quad * 8192 + sb * 4096;
                 if (lane == 0) bulk_wait_read<1>();   // previous store from this buffer has read it
                 __syncwarp();
@@ -343,7 +312,7 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
                     bulk_commit();
                 }
             }
-            if (row_ok) Wc[(((int64_t)bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = st.y;
+            if (row_ok) Wc[(((int64_t)tk.bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = c_l;
             if (lane == 0 && warp < 8) TR(warp, ti, 32);
         }
         if (lane == 0) bulk_wait<0>();
