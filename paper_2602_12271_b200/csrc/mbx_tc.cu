@@ -12,6 +12,7 @@
 
 #include <cuda.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 namespace mbx {
@@ -22,7 +23,6 @@ using namespace sm100;
 constexpr int kD = 128;           // head dim (q, k) and value dim
 constexpr int kMaxS2 = 64;        // tile-row tokens (MMA1 N, MMA2 K)
 constexpr int kMaxS1 = 32;        // tile rows (column-stage N)
-constexpr int kMaxGq = 3;         // query tiles per key row (M tile 0: a=0,1; M tile 1: a=2)
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t ring_parity(uint32_t n, uint32_t size) { return (n / size) & 1u; }
@@ -42,12 +42,82 @@ __device__ __forceinline__ void trace_ev(int role, int& idx, int tag) {
     }
 }
 #define TR(role, idx, tag) trace_ev(role, idx, tag)
+// Start / end timestamps of every CTA of the last launch of each kernel: [kernel][cta][2].
+constexpr int kSpanCtas = 256;
+__device__ unsigned long long g_span[2][kSpanCtas][2];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SPAN_AT(kern, which) \
+    do { if (threadIdx.x == 0 && blockIdx.x < kSpanCtas) g_span[kern][blockIdx.x][which] = gtimer(); } while (0)
 #else
 #define TR(role, idx, tag) ((void)0)
+#define SPAN_AT(kern, which) ((void)0)
 #endif
+#define SPAN_BEGIN() SPAN_AT(0, 0)
+#define SPAN_END() SPAN_AT(0, 1)
+
+// Every tensor map and pointer of one forward (kernel parameter, 64-byte aligned maps).
+struct TcParams {
+    CUtensorMap tq, tk, tv, tws, tws_b;   // row stage: q/k/v rows, workspace store boxes
+    CUtensorMap tw, tc, tqc, tout;        // column stage: workspace, c_L, q columns, output columns
+    float* wc;                            // c_L [col][ckey_stride]
+    const __nv_bfloat16* w;               // workspace W[col][part][key][64]
+    int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
+};
+
+// Row-stage query groups (<= 3 query tiles each) and key tiles per item; an
+// exchange unit is (bh, query group, key-tile chunk) and is complete after
+// unit_signals(g) releases (12 per item: 4 softmax + 8 epilogue warps, s1 items).
+__host__ __device__ __forceinline__ int row_groups(const Geometry& g) { return (g.gq + 2) / 3; }
+__host__ __device__ __forceinline__ int row_chunk(const Geometry& g) {
+    const int n = (g.gk + 6) / 7;
+    return (g.gk + n - 1) / n;
+}
+__host__ __device__ __forceinline__ unsigned unit_signals(const Geometry& g) { return 12u * (unsigned)g.s1; }
+__host__ __device__ __forceinline__ int exchange_units(const Geometry& g) {
+    const int cpi = row_chunk(g);
+    return g.bh * row_groups(g) * ((g.gk + cpi - 1) / cpi);
+}
 
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
+
+__device__ __forceinline__ uint8_t* aligned_smem() {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+}
+
+__global__ void __launch_bounds__(kRowThreads, 1) tc_row_stage(const __grid_constant__ TcParams P, Geometry g) {
+    SPAN_AT(0, 0);
+    row_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr);
+    SPAN_AT(0, 1);
+}
+
+__global__ void __launch_bounds__(kColThreads, 1) tc_column_stage(const __grid_constant__ TcParams P, Geometry g) {
+    SPAN_AT(1, 0);
+    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr);
+    SPAN_AT(1, 1);
+}
+
+// One launch, both stages: CTAs [0, n_row) run the row stage, the rest the column
+// stage, which consumes each exchange unit as soon as its counter completes --
+// while the unit is still L2-resident -- and then discards its lines.  Needs all
+// CTAs co-resident (cooperative launch, one CTA per SM).
+__global__ void __launch_bounds__(kRowThreads, 1)
+tc_fused(const __grid_constant__ TcParams P, Geometry g, int n_row, unsigned* counters) {
+    if ((int)blockIdx.x < n_row) {
+        SPAN_AT(0, 0);
+        row_role(aligned_smem(), P, g, blockIdx.x, n_row, counters);
+        SPAN_AT(0, 1);
+    } else {
+        SPAN_AT(1, 0);
+        col_role(aligned_smem(), P, g, blockIdx.x - n_row, gridDim.x - n_row, counters);
+        SPAN_AT(1, 1);
+    }
+}
 
 // ===================================================================== host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -130,12 +200,22 @@ bool column_grid(const Geometry& g, int* F, int* H, int* W) {
     return true;
 }
 
+// MBX_FUSED=1 selects the single-launch path; MBX_ROW_CTAS sets its row-stage CTA count.
+bool fused_enabled() {
+    const char* e = getenv("MBX_FUSED");
+    return e && e[0] == '1';
+}
+int row_ctas_override() {
+    const char* e = getenv("MBX_ROW_CTAS");
+    return e ? atoi(e) : 0;
+}
+
 }  // namespace
 
 bool tc_supported(const Geometry& g, int dtype, int flags) {
     if (flags & MBX_FLAG_FORCE_GENERIC) return false;
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T != 1) return false;
-    if (g.s2 > kMaxS2 || g.s1 > kMaxS1 || g.gq > kMaxGq) return false;
+    if (g.s2 > kMaxS2 || g.s1 > kMaxS1) return false;
     if (g.nf == 0 && (g.q_order || g.kv_order)) return false;   // rows need a closed form
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return false;
@@ -148,7 +228,8 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
 
 size_t tc_workspace_bytes(const Geometry& g) {
     const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
-    return align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4);
+    return align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4) +
+           align256((size_t)exchange_units(g) * 4);
 }
 
 cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
@@ -164,55 +245,81 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
         return cudaErrorInvalidValue;
-    CUtensorMap tq, tk, tv, tqc, tw, tws, tws_b, tc, tout;
-    if (!make_rows_map(&tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&tk, k, B, g.heads, nk, g.ks, g.s2) ||
-        !make_rows_map(&tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&tqc, q, g, nq) ||
-        !make_outcol_map(&tout, out, g, nq))
+    TcParams P;
+    {
+        const char* e = getenv("MBX_DBG");
+        P.dbg = e ? atoi(e) : 0;
+    }
+    if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, g.s2) ||
+        !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&P.tqc, q, g, nq) ||
+        !make_outcol_map(&P.tout, out, g, nq))
         return cudaErrorInvalidValue;
     const int64_t ncols = (int64_t)g.bh * g.gq * g.s2;
     const int64_t rows = ncols * g.nkeys;
     __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(workspace);
     float* Wc = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256(rows * 512));
+    unsigned* counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Wc) +
+                                                     align256((size_t)ncols * ckey_stride(g) * 4));
+    P.wc = Wc;
+    P.w = Wp;
     {
         // blocked W[col][part][key][64]: part 0,1 = aL halves, 2,3 = Y halves
         cuuint64_t dims[4] = {64, (cuuint64_t)g.nkeys, 4, (cuuint64_t)ncols};
         cuuint64_t strides[3] = {128, (cuuint64_t)g.nkeys * 128, (cuuint64_t)g.nkeys * 512};
         cuuint32_t box[4] = {64, (cuuint32_t)kKC, 1, 1};          // column stage: contiguous 12 KB
-        if (!encode(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+        if (!encode(&P.tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         // row stage: one key, the columns j of one epilogue warp (rows 0..31 and 32..s2-1)
         cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 32 ? g.s2 : 32)};
-        if (!encode(&tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
+        if (!encode(&P.tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
-        if (!encode(&tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
+        if (!encode(&P.tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
-        if (!encode(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
+        if (!encode(&P.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
             return cudaErrorInvalidValue;
     }
 
     cudaError_t e;
     const int smem_row = RowSmem::kTotal + 1024;
     const int smem_col = ColSmem::kTotal + 1024;
+    const int smem_fused = smem_row > smem_col ? smem_row : smem_col;
     if ((e = cudaFuncSetAttribute(tc_row_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_row)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(tc_column_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_col)) !=
         cudaSuccess)
         return e;
-    const int items = g.bh * g.s1 * ((g.gq + 1) / 2);   // row-stage items (b, h, k, M tile)
-    const int grid_row = items < num_sms() ? items : num_sms();
+    if ((e = cudaFuncSetAttribute(tc_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fused)) != cudaSuccess)
+        return e;
+
+    const int sms = num_sms();
+    if (fused_enabled()) {
+        // split of the SMs between the stages (MBX_ROW_CTAS overrides)
+        int n_row = row_ctas_override();
+        if (n_row <= 0) n_row = (int)(sms * 0.55);
+        if (n_row < 1) n_row = 1;
+        if (n_row > sms - 1) n_row = sms - 1;
+        if ((e = cudaMemsetAsync(counters, 0, (size_t)exchange_units(g) * 4, stream)) != cudaSuccess) return e;
+        void* args[] = {(void*)&P, (void*)&g, (void*)&n_row, (void*)&counters};
+        ProfScope p("tc_fused", stream);
+        e = cudaLaunchCooperativeKernel((const void*)tc_fused, dim3(sms), dim3(kRowThreads), args, smem_fused, stream);
+        if (e == cudaSuccess) return cudaGetLastError();
+        cudaGetLastError();   // not co-resident here: fall back to two launches
+    }
+    const int64_t key_rows = (int64_t)g.bh * g.s1 * row_groups(g) * g.gk;   // row-stage key rows
+    const int grid_row = key_rows < sms ? (int)key_rows : sms;
     {
         ProfScope p("tc_row_stage", stream);
-        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(tq, tk, tv, tws, tws_b, g, Wc);
+        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(P, g);
     }
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
-    const int grid_col = ngroups < num_sms() ? (int)ngroups : num_sms();
+    const int grid_col = ngroups < sms ? (int)ngroups : sms;
     {
         ProfScope p("tc_column_stage", stream);
-        tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(tw, tc, tqc, tout, g);
+        tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(P, g);
     }
     return cudaGetLastError();
 }
@@ -228,5 +335,11 @@ extern "C" int mbx_trace_dump(void* host, size_t bytes) {
     static unsigned long long zeros[4 * 16 * 2048];
     cudaMemcpyToSymbol(mbx::g_trace, zeros, sizeof(zeros));
     return (int)sizeof(mbx::g_trace);
+}
+extern "C" int mbx_span_dump(void* host, size_t bytes) {
+    if (bytes < sizeof(mbx::g_span)) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host, mbx::g_span, sizeof(mbx::g_span));
+    return (int)sizeof(mbx::g_span);
 }
 #endif

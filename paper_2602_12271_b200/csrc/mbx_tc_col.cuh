@@ -29,11 +29,26 @@ struct ColSmem {
     static constexpr int kTotal = kTmemSlot + 16;
 };
 
-__global__ void __launch_bounds__(kColThreads, 1)
-tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_c,
-                const __grid_constant__ CUtensorMap tm_qc, const __grid_constant__ CUtensorMap tm_out, Geometry g) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+// Waits until exchange unit u has all its row-stage signals, then orders the
+// subsequent TMA (async-proxy) reads after them.
+__device__ __forceinline__ void unit_wait(const unsigned* counters, int u, unsigned target) {
+    unsigned v;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counters + u) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Column-stage role of CTA `first` among `stride` column CTAs.  counters != nullptr:
+// wait for each exchange unit before reading it and discard its L2 lines after use.
+__device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
+                                         const unsigned* counters) {
+    const CUtensorMap& tm_w = P.tw;
+    const CUtensorMap& tm_c = P.tc;
+    const CUtensorMap& tm_qc = P.tqc;
+    const CUtensorMap& tm_out = P.tout;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ColSmem::kBars);
     uint64_t* ring_full = bars;                   // [6]
     uint64_t* ring_empty = bars + kRing;          // [6]
@@ -56,7 +71,6 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
     const int gpt = (g.s2 + 3) >> 2;                       // column groups per query tile
     const int groups = g.bh * g.gq * gpt;
     const int nch = (g.nkeys + kKC - 1) / kKC;
-    const int first = blockIdx.x, stride = gridDim.x;
     const int my_groups = first < groups ? (groups - first + stride - 1) / stride : 0;
 
     if (tid == 0) {
@@ -115,9 +129,17 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     tma_load_4d(dst + 16384, &tm_qc, q_full, 64, wcol, wrow, bh);
                 }
                 const int col0 = (bh * g.gq + a) * g.s2 + j0;
+                int cc_done = -1;
                 for (int ch = 0; ch < nch; ++ch) {
                     const int u = gi * nch + ch;
                     const int k0 = ch * kKC;
+                    if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
+                        const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
+                        const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
+                        const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
+                        for (int cc = cc_done + 1; cc <= cc_hi; ++cc) unit_wait(counters, ubase + cc, unit_signals(g));
+                        cc_done = cc_hi;
+                    }
                     for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
                         const int slot = n % kRing;
                         TR(8, ti, 1);
@@ -199,7 +221,7 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                 }
             }
         }
-    } else {
+    } else if (warp < 6) {
         // ------------------------------------------------------ softmax (warp i = column i) + output
         const int quad = warp & 3;                       // column i within the group == lane quadrant
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -277,26 +299,25 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     }
                     named_sync(1, 128);
                 }
-                // P_i row l (bf16, K-major SW128: keys 0-63 chunk 0, keys 64-95 chunk 1)
-                uint32_t pk[kKC / 2];
+                // P_i row l (bf16, K-major SW128: keys 0-63 chunk 0, keys 64-95 chunk 1), written
+                // 8 keys at a time so only one 16-byte group of packed values is live
+                if (u > 0) mbar_wait(&o_done[quad], (u - 1) & 1);   // MMA_O_i(u-1) done with P_i
                 float sq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int k = 0; k < kKC; k += 2) {
-                    const float p0 = ex2(x[k] - m_run), p1 = ex2(x[k + 1] - m_run);
-                    sq[(k >> 1) & 3] += p0 + p1;
-                    pk[k >> 1] = pack_bf16(p0, p1);
+                for (int cc = 0; cc < kKC / 8; ++cc) {
+                    uint32_t pk[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int k = cc * 8 + 2 * e;
+                        const float p0 = ex2(x[k] - m_run), p1 = ex2(x[k + 1] - m_run);
+                        sq[e] += p0 + p1;
+                        pk[e] = pack_bf16(p0, p1);
+                    }
+                    const uint32_t dst = sP + (cc >> 3) * 4096 + l * 128 + (((cc & 7) ^ (l & 7)) << 4);
+                    st_shared_v4(dst, pk[0], pk[1], pk[2], pk[3]);
                 }
                 const float sum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
                 s_run += sum;
-                if (u > 0) mbar_wait(&o_done[quad], (u - 1) & 1);   // MMA_O_i(u-1) done with P_i
-#pragma unroll
-                for (int cc = 0; cc < 8; ++cc)
-                    st_shared_v4(sP + l * 128 + ((cc ^ (l & 7)) << 4), pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2],
-                                 pk[4 * cc + 3]);
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc)
-                    st_shared_v4(sP + 4096 + l * 128 + ((cc ^ (l & 7)) << 4), pk[32 + 4 * cc], pk[33 + 4 * cc],
-                                 pk[34 + 4 * cc], pk[35 + 4 * cc]);
                 fence_proxy_async_smem();
                 mbar_arrive(&p_full[quad]);
                 if (lane == 0) TR(warp + 8, ti, 23);
@@ -351,6 +372,15 @@ tc_column_stage(const __grid_constant__ CUtensorMap tm_w, const __grid_constant_
                     }
                 }
                 if (lane == 0) TR(warp + 8, ti, 29);
+            }
+            if (counters) {   // this group's workspace lines are dead: drop them from L2 unwritten
+                for (int i = 0; i < 4; ++i) {
+                    if (j0 + i >= g.s2) break;
+                    const char* base = reinterpret_cast<const char*>(P.w) +
+                                       (size_t)((bh * g.gq + a) * g.s2 + j0 + i) * g.nkeys * 512 + quad * g.nkeys * 128;
+                    for (int ln = lane; ln < g.nkeys; ln += 32)
+                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (size_t)ln * 128) : "memory");
+                }
             }
             tc_fence_before();
             if (lane == 0) TR(warp + 8, ti, 27);

@@ -1,49 +1,112 @@
 // Row stage (included by mbx_tc.cu).
 //
-// Item = (b, h, in-tile row k, M-tile mt): the Q rows k of query tiles
-// 2mt, 2mt+1 (one 128-row M tile) stay in smem while the K/V rows k of every
-// key tile c stream through a 2-stage TMA ring.  Per task (key tile c):
-//   MMA1  S[(a,j), i] = Q_k . K_ck^T        128 x 64 x 128      -> TMEM buffer t%2
-//   softmax_i (warps 2-5, one query row per thread), c_L = sum R z - lse,
-//   R = p / l written as bf16 P (double-buffered)
-//   MMA2  [aL | Y]    = P . [K_ck | V_ck]   128 x 256 x 64      -> same TMEM buffer
-//   epilogue (warps 6-9): TMEM -> bf16 -> per-warp smem staging -> TMA store into the
-//   blocked workspace W[col][part][key][64] (part 0,1 = aL halves, 2,3 = Y halves),
-//   so the column stage reads contiguous 12 KB boxes.
+// Item = (b, h, in-tile row k, query group qg): the Q rows k of up to three query
+// tiles 3qg.. are copied (tcgen05.cp) from a smem staging tile into TMEM, where
+// they are the A operand of every MMA1 of the item; the K/V rows k of the item's
+// key tiles c stream through a 3-stage TMA ring and each serves the item's one or
+// two M tiles (tiles 3qg,3qg+1 | 3qg+2).  Per task (key tile c, M tile mt):
+//   MMA1  S[(a,j), i] = Q_k . K_ck^T        128 x 64 x 128  (A: TMEM, B: smem) -> S/P buffer t%2
+//   softmax_i (warps 2-5, one query row per thread), c_L = sum R z - lse straight to the
+//   workspace, R = p / l written back over S as packed bf16 P (tcgen05.st)
+//   MMA2a aL = P . K_ck                     128 x 128 x 64  (A = P in TMEM)  -> O_aL
+//   MMA2b Y  = P . V_ck                     128 x 128 x 64                   -> O_Y
+//   epilogue: warps 6-9 drain O_aL, warps 10-13 drain O_Y: TMEM -> bf16 -> per-warp
+//   SW128 staging -> TMA store into the blocked workspace W[col][part][key][64]
+//   (part 0,1 = aL halves, 2,3 = Y halves).
+// The MMA warp issues MMA1 and MMA2 in readiness order from two independent
+// cursors, so the tensor pipe never idles behind one stage's wait.
 // (solver.py:187-191 R update and c_L; factors.py:123 Y = R V; tensorops.py:268-272)
-constexpr int kRowThreads = 320;   // 10 warps
+constexpr int kRowThreads = 448;   // 14 warps
+constexpr int kQG = 3;             // query tiles per item
+constexpr int kKVStages = 3;
 struct RowSmem {
-    // Q[2] (32 KB each): d-chunk c at c*16K, query tile 2mt+la at rows la*64.. (+la*8K)
+    // Q staging (48 KB): [d-chunk 2][query tile 3][64 rows][128 B], SW128 (tcgen05.cp source)
     static constexpr int kQ = 0;
-    static constexpr int kQBytes = 32768;
-    static constexpr int kKV = 2 * kQBytes;           // KV[2]: [K c0 | K c1 | V c0 | V c1] 8 KB each (32 KB)
+    static constexpr int kQChunk = kQG * 8192;
+    static constexpr int kQBytes = 2 * kQChunk;
+    static constexpr int kKV = kQBytes;               // KV[3]: [K c0 | K c1 | V c0 | V c1] 8 KB each
     static constexpr int kKVBytes = 32768;
-    static constexpr int kP = kKV + 2 * kKVBytes;     // P[2]: [128][64] bf16 (16 KB each)
-    static constexpr int kStage = kP + 2 * 16384;     // epilogue staging [4 warps][2] x [32][64] bf16 (4 KB each)
-    static constexpr int kStats = kStage + 2 * 16384; // c_L[2][128] floats
-    static constexpr int kBars = kStats + 2 * 128 * 4;
-    static constexpr int kNumBars = 18;
+    static constexpr int kStage = kKV + kKVStages * kKVBytes;   // staging [8 warps][2] x [32][64] bf16
+    static constexpr int kBars = kStage + 16 * 4096;
+    static constexpr int kNumBars = 2 + 2 * kKVStages + 2 + 2 + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
+static_assert(RowSmem::kTotal + 1024 <= 232448, "row stage exceeds 227 KB of shared memory");
 
-struct RowTask {            // decoded task t of this CTA: item (b,h,k,mt), key tile c
-    int bh, kr, mt, c;
-    bool first_of_item, last_of_item;
+// TMEM columns: Q M tiles [0,64) [64,128); S/P buffers [128,192) [192,256); O_aL [256,384); O_Y [384,512).
+constexpr uint32_t kRowQ = 0, kRowS = 128, kRowO = 256;
+
+// Walks the (item, key tile c, M tile mt) task sequence of one CTA.  Items are
+// ordered (b*h, query group qg, key-tile chunk cc, row k).  Two schedules:
+//  * round-robin items (single-launch path): the CTAs advance through the exchange
+//    units u = (bh, qg, cc) together, so each unit is consumed while L2-resident;
+//  * a contiguous range [L0, L1) of key rows (two-launch path; one chunk per item):
+//    equal key-row counts per CTA, the item's Q reloaded only at item boundaries.
+struct RowCursor {
+    int li, c, mt, kvi, n_mt, nt, bh, kr, qg, cc, c0, c1, unit, my_items, first, stride, n_qg, n_cc, cpi;
+    int L0, L1;   // range schedule (stride == 0)
+    int kst, kph; // K/V ring stage (kvi % kKVStages) and its phase parity, kept incrementally
+    bool valid;
+    __device__ __forceinline__ void load(const Geometry& g) {
+        valid = li < my_items;
+        if (!valid) return;
+        const int item = stride ? first + li * stride : L0 / cpi + li;
+        kr = item % g.s1;
+        unit = item / g.s1;
+        cc = unit % n_cc;
+        qg = (unit / n_cc) % n_qg;
+        bh = unit / (n_cc * n_qg);
+        nt = min(kQG, g.gq - kQG * qg);
+        n_mt = (nt + 1) >> 1;
+        c0 = cc * cpi;
+        c1 = min(g.gk, c0 + cpi);
+        if (!stride) {
+            if (li == 0) c0 = L0 % cpi;
+            if (li == my_items - 1) c1 = (L1 - 1) % cpi + 1;
+        }
+        c = c0;
+    }
+    __device__ __forceinline__ void init(const Geometry& g, int first_, int stride_) {
+        first = first_;
+        stride = stride_;
+        n_qg = row_groups(g);
+        cpi = row_chunk(g);
+        n_cc = (g.gk + cpi - 1) / cpi;
+        const int items = g.bh * n_qg * n_cc * g.s1;
+        my_items = first < items ? (items - first + stride - 1) / stride : 0;
+        li = mt = kvi = kst = kph = 0;
+        load(g);
+    }
+    // Range schedule: CTA `cta` of `ctas` takes an equal share of all key rows.
+    __device__ __forceinline__ void init_range(const Geometry& g, int cta, int ctas) {
+        stride = 0;
+        first = 0;
+        n_qg = row_groups(g);
+        cpi = g.gk;
+        n_cc = 1;
+        const long long rows = (long long)g.bh * n_qg * g.s1 * g.gk;
+        L0 = (int)(rows * cta / ctas);
+        L1 = (int)(rows * (cta + 1) / ctas);
+        my_items = L1 > L0 ? (L1 - 1) / cpi - L0 / cpi + 1 : 0;
+        li = mt = kvi = kst = kph = 0;
+        load(g);
+    }
+    __device__ __forceinline__ bool last_mt() const { return mt == n_mt - 1; }
+    __device__ __forceinline__ bool last_of_item() const { return last_mt() && c == c1 - 1; }
+    __device__ __forceinline__ void advance(const Geometry& g) {
+        if (++mt < n_mt) return;
+        mt = 0;
+        ++kvi;
+        if (++kst == kKVStages) {
+            kst = 0;
+            kph ^= 1;
+        }
+        if (++c < c1) return;
+        ++li;
+        load(g);
+    }
 };
-
-__device__ __forceinline__ RowTask row_task(const Geometry& g, int t, int n_mt, int first_item, int item_stride) {
-    RowTask r;
-    const int li = t / g.gk;
-    r.c = t - li * g.gk;
-    const int item = first_item + li * item_stride;   // item = (bh * s1 + k) * n_mt + mt
-    r.mt = item % n_mt;
-    r.kr = (item / n_mt) % g.s1;
-    r.bh = item / (n_mt * g.s1);
-    r.first_of_item = r.c == 0;
-    r.last_of_item = r.c == g.gk - 1;
-    return r;
-}
 
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
     asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
@@ -57,32 +120,49 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 template <int N>
 __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(kRowThreads, 1)
-tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_wst,
-             const __grid_constant__ CUtensorMap tm_wst_b, Geometry g, float* __restrict__ Wc) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+// D[tmem] (+)= A[tmem] * B[smem]; issued by ONE thread.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            bool accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"((uint32_t)accumulate));
+}
+
+// Release one signal on exchange unit u (after this thread's / warp's writes of it).
+__device__ __forceinline__ void unit_signal(unsigned* counters, int u) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counters + u) : "memory");
+}
+
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+
+// Row-stage role of CTA `first` among `stride` row CTAs.  counters == nullptr: no
+// exchange signalling (two-launch path, contiguous key-row ranges).
+__device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
+                                         unsigned* counters) {
+    const CUtensorMap& tm_q = P.tq;
+    const CUtensorMap& tm_k = P.tk;
+    const CUtensorMap& tm_v = P.tv;
+    const CUtensorMap& tm_wst = P.tws;
+    const CUtensorMap& tm_wst_b = P.tws_b;
+    float* __restrict__ Wc = P.wc;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RowSmem::kBars);
-    uint64_t* q_full = bars + 0;    // [2]
-    uint64_t* q_empty = bars + 2;   // [2]
-    uint64_t* kv_full = bars + 4;   // [2]
-    uint64_t* kv_empty = bars + 6;  // [2]
-    uint64_t* s_full = bars + 8;    // [2]
-    uint64_t* o_full = bars + 10;   // [2]
-    uint64_t* t_empty = bars + 12;  // [2]
-    uint64_t* p_full = bars + 14;   // [2]
-    uint64_t* p_empty = bars + 16;  // [2]
-    float* stats = reinterpret_cast<float*>(smem + RowSmem::kStats);
+    uint64_t* q_full = bars + 0;                  // Q staging landed
+    uint64_t* q_empty = bars + 1;                 // Q staging copied into TMEM
+    uint64_t* kv_full = bars + 2;                 // [3]
+    uint64_t* kv_empty = kv_full + kKVStages;     // [3]
+    uint64_t* s_full = kv_empty + kKVStages;      // [2]
+    uint64_t* p_full = s_full + 2;                // [2]
+    uint64_t* o_full = p_full + 2;                // [2] O_aL / O_Y written
+    uint64_t* o_empty = o_full + 2;               // [2] O_aL / O_Y drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowSmem::kTmemSlot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    const int n_mt = (g.gq + 1) >> 1;
-    const int items = g.bh * g.s1 * n_mt;
-    const int first_item = blockIdx.x, item_stride = gridDim.x;
-    const int my_items = first_item < items ? (items - first_item + item_stride - 1) / item_stride : 0;
-    const int my_tasks = my_items * g.gk;
     const uint32_t box_bytes = (uint32_t)g.s2 * 128u;
+    const int ckey = ckey_stride(g);
 
     if (tid == 0) {
         tma_prefetch(&tm_q);
@@ -90,23 +170,26 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_wst);
         tma_prefetch(&tm_wst_b);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&q_full[i], 1);
-            mbar_init(&q_empty[i], 1);
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < kKVStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&o_full[i], 1);
-            mbar_init(&t_empty[i], 128);
             mbar_init(&p_full[i], 128);
-            mbar_init(&p_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 128);
         }
         fence_barrier_init();
     }
-    // Rows s2..63 of every box slot (and the second query-tile slot of an odd last
-    // M tile) are never written by TMA: zero them once so MMA padding reads zeros.
-    for (int i = tid; i < (2 * RowSmem::kQBytes + 2 * RowSmem::kKVBytes) / 16; i += kRowThreads)
-        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    // Rows s2..63 of the K/V slots are never written by TMA; MMA2 multiplies them by
+    // P = 0, so they must be finite: zero them once.
+    for (int i = tid; i < kKVStages * RowSmem::kKVBytes / 16; i += kRowThreads)
+        reinterpret_cast<uint4*>(smem + RowSmem::kKV)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tmem_alloc<512>(tmem_slot);
     fence_proxy_async_smem();
     tc_fence_before();
@@ -114,94 +197,143 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+#define WAITX(bar, par) do { if (P.dbg & 64) mbar_spin(bar, par); else if (P.dbg & 128) mbar_wait_nohint(bar, par); else mbar_wait(bar, par); } while (0)
+    RowCursor cur;
+    if (counters)
+        cur.init(g, first, stride);
+    else
+        cur.init_range(g, first, stride);
+
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
-            int ti = 0;
-            for (int t = 0; t < my_tasks; ++t) {
-                const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
-                const int b = tk.bh / g.heads, h = tk.bh % g.heads;
-                if (tk.first_of_item) {
-                    const int li = t / g.gk, qs = li & 1;
-                    mbar_wait(&q_empty[qs], ring_parity(li, 2) ^ 1);
-                    TR(0, ti, 1);
-                    const int nqa = min(2, g.gq - 2 * tk.mt);
-                    mbar_expect_tx(&q_full[qs], 2u * box_bytes * (uint32_t)nqa);
-                    uint8_t* qb = smem + RowSmem::kQ + qs * RowSmem::kQBytes;
-                    for (int la = 0; la < nqa; ++la) {
-                        const int tok = (int)row_base(g, true, 2 * tk.mt + la, tk.kr);
-                        tma_load_4d(qb + la * 8192, &tm_q, &q_full[qs], 0, tok, h, b);
-                        tma_load_4d(qb + 16384 + la * 8192, &tm_q, &q_full[qs], 64, tok, h, b);
-                    }
+            int ti = 0, kvi = 0;
+            // Q rows of item li into the staging tile (free once the previous item's Q was copied)
+            auto load_q = [&](int li) {
+                RowCursor qc = cur;
+                qc.li = li;
+                qc.load(g);
+                const int b = qc.bh / g.heads, h = qc.bh % g.heads;
+                WAITX(q_empty, (li & 1) ^ 1);
+                TR(0, ti, 1);
+                if ((P.dbg & 512) && li > 0) {   // timing experiment: reuse the staged Q rows
+                    mbar_arrive(q_full);
+                    return;
                 }
-                const int ks = t & 1;
-                mbar_wait(&kv_empty[ks], ring_parity(t, 2) ^ 1);
-                TR(0, ti, 2);
-                mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
-                uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
-                const int tok = (int)row_base(g, false, tk.c, tk.kr);
-                tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
-                tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
-                tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
-                tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                mbar_expect_tx(q_full, 2u * box_bytes * (uint32_t)qc.nt);
+                uint8_t* qb = smem + RowSmem::kQ;
+                for (int la = 0; la < qc.nt; ++la) {
+                    const int tok = (int)row_base(g, true, kQG * qc.qg + la, qc.kr);
+                    tma_load_4d(qb + la * 8192, &tm_q, q_full, 0, tok, h, b);
+                    tma_load_4d(qb + RowSmem::kQChunk + la * 8192, &tm_q, q_full, 64, tok, h, b);
+                }
+            };
+            if (cur.my_items > 0) load_q(0);
+            for (int li = 0; li < cur.my_items; ++li) {
+                cur.li = li;
+                cur.load(g);
+                const int b = cur.bh / g.heads, h = cur.bh % g.heads;
+                for (int c = cur.c0; c < cur.c1; ++c, ++kvi) {
+                    const int ks = kvi % kKVStages;
+                    WAITX(&kv_empty[ks], ring_parity(kvi, kKVStages) ^ 1);
+                    TR(0, ti, 2);
+                    if ((P.dbg & 8) && kvi >= kKVStages) {   // timing experiment: reuse resident K/V
+                        mbar_arrive(&kv_full[ks]);
+                        if (c == cur.c1 - 1 && li + 1 < cur.my_items) load_q(li + 1);
+                        continue;
+                    }
+                    mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
+                    uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
+                    const int tok = (int)row_base(g, false, c, cur.kr);
+                    tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
+                    tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
+                    tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
+                    tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                    if (c == ((P.dbg & 256) ? cur.c0 : cur.c1 - 1) && li + 1 < cur.my_items) load_q(li + 1);
+                }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------ MMA issuer
+        // ------------------------------------------------------ MMA issuer (readiness order)
+        // The single issuing thread is on the critical path: descriptors are precomputed
+        // (only the 14-bit start-address field moves) and ring positions kept incrementally.
         if (lane == 0) {
             const uint32_t idesc_s = idesc_bf16(128, 64, false, false);
-            const uint32_t idesc_o = idesc_bf16(128, 256, false, true);
+            const uint32_t idesc_o = idesc_bf16(128, 128, false, true);
+            constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
+            const uint32_t kv_lo = (smem_u32(smem + RowSmem::kKV) & 0x3FFFF) >> 4;
+            const uint32_t q_lo = ((smem_u32(smem + RowSmem::kQ) & 0x3FFFF) >> 4) | (1u << 16);
+            auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
             int ti = 0;
-            auto issue_s = [&](int t) {   // MMA1(t): TMEM buffer t%2 must be free
-                const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
-                const int li = t / g.gk;
-                if (tk.first_of_item) mbar_wait(&q_full[li & 1], ring_parity(li, 2));
-                mbar_wait(&kv_full[t & 1], ring_parity(t, 2));
-                TR(1, ti, 11);
-                tc_fence_after();
-                const uint32_t qbase = smem_u32(smem + RowSmem::kQ + (li & 1) * RowSmem::kQBytes);
-                const uint32_t kbase = smem_u32(smem + RowSmem::kKV + (t & 1) * RowSmem::kKVBytes);
+            RowCursor cs = cur, co = cur;   // next MMA1 task ts, next MMA2 task to
+            int ts = 0, to = 0, q_item = -1;
+            bool s_kv_ok = false;           // K/V of cs's key row known to have landed
+            while (cs.valid || co.valid) {
+                bool did = false;
+                // MMA2(to): softmax done with S/P buffer to%2, both O buffers drained by task to-1
+                if (co.valid && to < ts && ((P.dbg & 32) || (mbar_test(&p_full[to & 1], (to >> 1) & 1) &&
+                    mbar_test(&o_empty[0], (to & 1) ^ 1) && mbar_test(&o_empty[1], (to & 1) ^ 1)))) {
+                    TR(1, ti, 12);
+                    tc_fence_after();
+                    // B = [K | V] row, MN-major SW128 (LBO 8192 between 64-feature atoms)
+                    const uint32_t b_lo = kv_lo + (uint32_t)co.kst * (RowSmem::kKVBytes >> 4) + (8192u >> 4 << 16);
+                    const uint32_t pa = tmem + kRowS + (to & 1) * 64;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t ad = smem_desc(qbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
-                    const uint64_t bd = smem_desc(kbase + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2);
-                    mma_bf16(tmem + (t & 1) * 256, ad, bd, idesc_s, kk > 0);
-                }
-                mma_commit(&s_full[t & 1]);
-            };
-            if (my_tasks > 0) issue_s(0);
-            for (int t = 0; t < my_tasks; ++t) {
-                const RowTask cur = row_task(g, t, n_mt, first_item, item_stride);
-                // MMA1(t+1) waits for the epilogue of t-1 to free TMEM buffer (t+1)%2, MMA2(t)
-                // for softmax(t): issue whichever is ready first so neither chain stalls the other.
-                bool s_done = t + 1 >= my_tasks, o_done = false;
-                while (!o_done) {
-                    if (!s_done && mbar_test(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1)) {
-                        issue_s(t + 1);
-                        s_done = true;
+                    for (int s = 0; s < 2; ++s) {   // s = 0: aL = P K, s = 1: Y = P V
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_bf16_ts(tmem + kRowO + s * 128, pa + kk * 8,
+                                        desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), idesc_o, kk > 0);
+                        mma_commit(&o_full[s]);
                     }
-                    if (mbar_test(&p_full[t & 1], ring_parity(t, 2))) {
-                        TR(1, ti, 12);
-                        tc_fence_after();
-                        const uint32_t pbase = smem_u32(smem + RowSmem::kP + (t & 1) * 16384);
-                        const uint32_t kbase = smem_u32(smem + RowSmem::kKV + (t & 1) * RowSmem::kKVBytes);
+                    if (co.last_mt()) mma_commit(&kv_empty[co.kst]);
+                    co.advance(g);
+                    ++to;
+                    did = true;
+                }
+                // MMA1(ts): S/P buffer ts%2 released by MMA2(ts-2), Q of its item in TMEM, K/V landed
+                if (cs.valid && ts < to + 2) {
+                    bool ready = true;
+                    if (cs.li != q_item) {
+                        // first task of a new item: all MMA1 of the previous item are issued,
+                        // so (tensor-pipe order) the copy cannot overtake their reads of Q
+                        if (mbar_test(q_full, cs.li & 1)) {
+                            tc_fence_after();
+                            for (int mt = 0; mt < cs.n_mt; ++mt)
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t ad = smem_desc(pbase + kk * 32, 16, 1024, 2);
-                            const uint64_t bd = smem_desc(kbase + kk * 2048, 8192, 1024, 2);
-                            mma_bf16(tmem + (t & 1) * 256, ad, bd, idesc_o, kk > 0);
+                                for (int kk = 0; kk < 8; ++kk)
+                                    tmem_cp_128x256b(tmem + kRowQ + mt * 64 + kk * 8,
+                                                     desc(q_lo + (((kk >> 2) * RowSmem::kQChunk + mt * 16384 +
+                                                                   (kk & 3) * 32) >> 4)));
+                            mma_commit(q_empty);
+                            q_item = cs.li;
+                        } else {
+                            ready = false;
                         }
-                        mma_commit(&o_full[t & 1]);
-                        mma_commit(&p_empty[t & 1]);
-                        mma_commit(&kv_empty[t & 1]);
-                        if (cur.last_of_item) mma_commit(&q_empty[(t / g.gk) & 1]);
-                        o_done = true;
+                    }
+                    if (ready && cs.mt == 0 && !s_kv_ok) {
+                        s_kv_ok = mbar_test(&kv_full[cs.kst], cs.kph);
+                        ready = s_kv_ok;
+                    }
+                    if (ready) {
+                        TR(1, ti, 11);
+                        tc_fence_after();
+                        // B = K row, K-major SW128 (LBO 16)
+                        const uint32_t b_lo = kv_lo + (uint32_t)cs.kst * (RowSmem::kKVBytes >> 4) + (1u << 16);
+                        const uint32_t a_t = tmem + kRowQ + cs.mt * 64;
+                        const uint32_t d_t = tmem + kRowS + (ts & 1) * 64;
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk)
+                            mma_bf16_ts(d_t, a_t + kk * 8, desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)),
+                                        idesc_s, kk > 0);
+                        mma_commit(&s_full[ts & 1]);
+                        if (cs.last_mt()) s_kv_ok = false;
+                        cs.advance(g);
+                        ++ts;
+                        did = true;
                     }
                 }
-                if (!s_done) {
-                    mbar_wait(&t_empty[(t + 1) & 1], ring_parity(t + 1, 2) ^ 1);
-                    issue_s(t + 1);
-                }
+                if (!did) __nanosleep(20);
             }
         }
     } else if (warp < 6) {
@@ -211,111 +343,177 @@ tc_row_stage(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ C
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const float sl2 = g.scale * kLog2e;
         int ti = 0;
-        for (int t = 0; t < my_tasks; ++t) {
-            const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
+        for (int t = 0; cur.valid; ++t, cur.advance(g)) {
             const int bsel = t & 1;
-            const int a = tk.mt * 2 + (r >> 6), j = r & 63;
-            const bool row_ok = a < g.gq && j < g.s2;
-            mbar_wait(&s_full[bsel], ring_parity(t, 2));
+            const uint32_t sbuf = tmem + kRowS + bsel * 64 + lane_off;
+            const int al = cur.mt * 2 + (r >> 6), j = r & 63;
+            const bool row_ok = al < cur.nt && j < g.s2;
+            WAITX(&s_full[bsel], ring_parity(t, 2));
             if (lane == 0) TR(warp, ti, 21);
             tc_fence_after();
+            if (P.dbg & 4) {   // timing experiment: no softmax arithmetic
+                float zz[32];
+                for (int i = 0; i < 32; ++i) zz[i] = 0.f;
+                tmem_st32(sbuf, zz);
+                tc_fence_before();
+                mbar_arrive(&p_full[bsel]);
+                continue;
+            }
             float z[64];
-            tmem_ld32(tmem + bsel * 256 + lane_off, z);
-            tmem_ld32(tmem + bsel * 256 + lane_off + 32, z + 32);
+            {
+                uint32_t zr[64];
+                tmem_ld32_nw(sbuf, zr);
+                tmem_ld32_nw(sbuf + 32, zr + 32);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 64; ++i) z[i] = __uint_as_float(zr[i]);
+            }
             // padded keys -> -1e30 (finite: exp2 -> 0 and 0 * z stays 0)
-            if (g.s2 < 64) {
 #pragma unroll
-                for (int i = 0; i < 64; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+            for (int blk = 0; blk < 4; ++blk) {   // only the 16-column blocks that reach past s2
+                if (16 * blk + 16 > g.s2) {
+#pragma unroll
+                    for (int i = 16 * blk; i < 16 * blk + 16; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+                }
             }
-            float mq[4] = {-1e30f, -1e30f, -1e30f, -1e30f};
+            float mq[8];
 #pragma unroll
-            for (int i = 0; i < 64; ++i) mq[i & 3] = fmaxf(mq[i & 3], z[i]);
-            const float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+            for (int e = 0; e < 8; ++e) mq[e] = fmaxf(z[e], z[e + 8]);
+#pragma unroll
+            for (int i = 16; i < 64; i += 8)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mq[e] = fmaxf(mq[e], z[i + e]);
+            const float m = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                  fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
             const float mb = m * sl2;
-            float lq[4] = {0.f, 0.f, 0.f, 0.f}, aq[4] = {0.f, 0.f, 0.f, 0.f};
+            // p = 2^(z sl2 - m sl2); l = sum p; A = sum p z -- eight independent partial sums
+            float p[64];
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) {
-                const float p0 = ex2(fmaf(z[i], sl2, -mb)), p1 = ex2(fmaf(z[i + 1], sl2, -mb));
-                lq[(i >> 1) & 3] += p0 + p1;
-                aq[(i >> 1) & 3] = fmaf(p1, z[i + 1], fmaf(p0, z[i], aq[(i >> 1) & 3]));
-                z[i] = p0;
-                z[i + 1] = p1;
+            for (int i = 0; i < 64; ++i) p[i] = ex2(fmaf(z[i], sl2, -mb));
+            float lq[8], aq[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                lq[e] = p[e] + p[e + 8];
+                aq[e] = fmaf(p[e + 8], z[e + 8], p[e] * z[e]);
             }
-            const float l = (lq[0] + lq[1]) + (lq[2] + lq[3]);
-            const float A = (aq[0] + aq[1]) + (aq[2] + aq[3]);
+#pragma unroll
+            for (int i = 16; i < 64; i += 8)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    lq[e] += p[i + e];
+                    aq[e] = fmaf(p[i + e], z[i + e], aq[e]);
+                }
+            const float l = ((lq[0] + lq[1]) + (lq[2] + lq[3])) + ((lq[4] + lq[5]) + (lq[6] + lq[7]));
+            const float A = ((aq[0] + aq[1]) + (aq[2] + aq[3])) + ((aq[4] + aq[5]) + (aq[6] + aq[7]));
             const float inv_l = 1.f / l;
-            // c_L = sum R z - lse with z = scale * S
-            stats[bsel * 128 + r] = g.scale * (A * inv_l - m) - __logf(l);
-            // R = p / l goes into P (bf16, <= 1), so MMA2 yields normalised aL and Y
+            // R = p / l (bf16, <= 1) over S's first 32 columns: MMA2 reads it as its A operand
             const float pscale = row_ok ? inv_l : 0.f;
             uint32_t packed[32];
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(z[i] * pscale, z[i + 1] * pscale);
+            for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(p[i] * pscale, p[i + 1] * pscale);
+            tmem_st32(sbuf, reinterpret_cast<const float*>(packed));
             tc_fence_before();
-            mbar_wait(&p_empty[bsel], ring_parity(t, 2) ^ 1);   // MMA2(t-2) done with P[bsel]
-            const uint32_t p_row = smem_u32(smem + RowSmem::kP + bsel * 16384) + r * 128;
-#pragma unroll
-            for (int cc = 0; cc < 8; ++cc)
-                st_shared_v4(p_row + ((cc ^ (r & 7)) << 4), packed[4 * cc], packed[4 * cc + 1],
-                             packed[4 * cc + 2], packed[4 * cc + 3]);
-            fence_proxy_async_smem();
             mbar_arrive(&p_full[bsel]);
+            // c_L = sum R z - lse with z = scale * S (solver.py:191)
+            if (row_ok) {
+                const int col = (cur.bh * g.gq + kQG * cur.qg + al) * g.s2 + j;
+                Wc[(int64_t)col * ckey + cur.c * g.s1 + cur.kr] = g.scale * (A * inv_l - m) - __logf(l);
+            }
+            if (counters && cur.last_of_item()) {   // this warp's c_L of the item are written
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) unit_signal(counters, cur.unit);
+            }
             if (lane == 0) TR(warp, ti, 22);
         }
     } else {
         // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
+        const int set = warp >= 10 ? 1 : 0;   // warps 6-9: O_aL (quarters 0,1), 10-13: O_Y (2,3)
         const int quad = warp & 3;
-        const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        int nstore = 0;   // staging buffer uses of this warp
+        const uint32_t obuf = tmem + kRowO + set * 128 + lane_off;
+        const int half = quad & 1;
+        const int nrows = min(32, g.s2 - half * 32);
+        uint8_t* stg_base = smem + RowSmem::kStage + (warp - 6) * 8192;
+        int nstore = 0;   // staging buffer uses (== bulk groups committed) of this warp
         int ti = 0;
-        for (int t = 0; t < my_tasks; ++t) {
-            const RowTask tk = row_task(g, t, n_mt, first_item, item_stride);
-            const int bsel = t & 1;
-            const int a = tk.mt * 2 + (r >> 6), j = r & 63;
-            const bool row_ok = a < g.gq && j < g.s2;
-            const int key = tk.c * g.s1 + tk.kr;
-            mbar_wait(&o_full[bsel], ring_parity(t, 2));
-            if (lane == 0 && warp < 8) TR(warp, ti, 31);
+        // An item is signalled once its TMA stores have completed; to keep stores in
+        // flight the wait is deferred until two newer groups exist (or forced).
+        int pend_u = -1, pend_g = 0;
+        auto flush = [&](bool force) {
+            if (pend_u < 0) return;
+            if (nstore - pend_g >= 2) {
+                if (lane == 0) bulk_wait<2>();
+            } else if (force) {
+                if (lane == 0) bulk_wait<0>();
+            } else {
+                return;
+            }
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                unit_signal(counters, pend_u);
+            }
+            pend_u = -1;
+        };
+        for (int t = 0; cur.valid; ++t, cur.advance(g)) {
+            const int al = cur.mt * 2 + (quad >> 1);
+            const bool store_ok = al < cur.nt && nrows > 0;
+            const int key = cur.c * g.s1 + cur.kr;
+            const int col0 = (cur.bh * g.gq + kQG * cur.qg + (al < cur.nt ? al : 0)) * g.s2 + half * 32;
+            mbar_wait(&o_full[set], t & 1);
+            if (lane == 0) TR(warp, ti, 31);
             tc_fence_after();
-            const float c_l = stats[bsel * 128 + r];
-            // per-warp staging (32 rows x 64 features) and per-warp TMA store: no cross-warp sync
-            const int half = quad & 1;
-            const int nrows = min(32, g.s2 - half * 32);
-            const bool store_ok = a < g.gq && nrows > 0;
-            const int col0 = (tk.bh * g.gq + (a < g.gq ? a : 0)) * g.s2 + half * 32;
-            for (int part = 0; part < 4; ++part) {
-                float o[64];
-                tmem_ld32(tmem + bsel * 256 + lane_off + part * 64, o);
-                tmem_ld32(tmem + bsel * 256 + lane_off + part * 64 + 32, o + 32);
-                if (part == 3) {   // TMEM buffer fully read: MMA1(t+2) may reuse it
-                    tc_fence_before();
-                    mbar_arrive(&t_empty[bsel]);
-                }
-                // a warp whose rows are all padding (a >= G_q) writes nothing: touching the
-                // staging buffer would race with this warp's in-flight TMA store from it
-                if (!store_ok) continue;
-                const int sb = nstore++ & 1;
-                uint8_t* stg = smem + RowSmem::kStage + quad * 8192 + sb * 4096;
-                if (lane == 0) bulk_wait_read<1>();   // previous store from this buffer has read it
-                __syncwarp();
-                const uint32_t srow = smem_u32(stg) + lane * 128;
+            if (P.dbg & 2) {   // timing experiment: no drain
+                tc_fence_before();
+                mbar_arrive(&o_empty[set]);
+                continue;
+            }
+            // both 64-feature parts to registers as packed bf16, then release the buffer
+            uint32_t pk[2][32];
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc)
-                    st_shared_v4(srow + ((cc ^ (lane & 7)) << 4),
-                                 pack_bf16(o[8 * cc], o[8 * cc + 1]), pack_bf16(o[8 * cc + 2], o[8 * cc + 3]),
-                                 pack_bf16(o[8 * cc + 4], o[8 * cc + 5]), pack_bf16(o[8 * cc + 6], o[8 * cc + 7]));
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store_4d(half ? &tm_wst_b : &tm_wst, stg, 0, key, part, col0);
-                    bulk_commit();
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t o[32];
+                tmem_ld32_nw(obuf + q4 * 32, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    pk[q4 >> 1][(q4 & 1) * 16 + i] = pack_bf16(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+            }
+            tc_fence_before();
+            mbar_arrive(&o_empty[set]);
+            // a warp whose rows are all padding writes nothing: touching the staging
+            // buffer would race with this warp's in-flight TMA store from it
+            if (store_ok && !(P.dbg & 1)) {
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    uint8_t* stg = stg_base + (nstore++ & 1) * 4096;
+                    if (lane == 0) bulk_wait_read<1>();   // previous store from this buffer has read it
+                    __syncwarp();
+                    const uint32_t srow = smem_u32(stg) + lane * 128;
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc)
+                        st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pk[part][4 * cc], pk[part][4 * cc + 1],
+                                     pk[part][4 * cc + 2], pk[part][4 * cc + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_4d(half ? &tm_wst_b : &tm_wst, stg, 0, key, 2 * set + part, col0);
+                        bulk_commit();
+                    }
                 }
             }
-            if (row_ok) Wc[(((int64_t)tk.bh * g.gq + a) * g.s2 + j) * ckey_stride(g) + key] = c_l;
-            if (lane == 0 && warp < 8) TR(warp, ti, 32);
+            if (counters) {
+                flush(false);
+                if (cur.last_of_item()) {
+                    flush(true);   // at most one item pending
+                    pend_u = cur.unit;
+                    pend_g = nstore;
+                }
+            }
+            if (lane == 0 && warp < 16) TR(warp, ti, 32);
         }
         if (lane == 0) bulk_wait<0>();
+        if (counters) flush(true);
     }
     tc_fence_before();
     __syncthreads();

@@ -26,6 +26,18 @@ for it in range(3):
     torch.cuda.synchronize()
     lib.mbx_trace_dump(buf.ctypes.data, buf.nbytes)   # keep only the last run's trace
 ev = buf.reshape(4, 16, 2048)
+lib.mbx_span_dump.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+span = np.zeros(2 * 256 * 2, dtype=np.uint64)
+lib.mbx_span_dump(span.ctypes.data, span.nbytes)
+span = span.reshape(2, 256, 2).astype(np.int64)
+t0s = span[0, :, 0][span[0, :, 0] > 0].min()
+for kern, name in ((0, "row"), (1, "col")):
+    ok = span[kern, :, 0] > 0
+    st = (span[kern, ok, 0] - t0s) / 1000.0
+    en = (span[kern, ok, 1] - t0s) / 1000.0
+    print(f"span {name}: ctas {ok.sum()} start min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f} "
+          f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f} us")
+    print("  ends:", " ".join(f"{x:.1f}" for x in np.sort(en)[:: max(1, len(en) // 24)]))
 for cta in range(int(os.environ.get("NCTA", "1"))):
     allt = [int(x) >> 8 for x in ev[cta].ravel() if x]
     t0 = min(allt) if allt else 0
