@@ -63,8 +63,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct TcParams {
     CUtensorMap tq, tk, tv, tws, tws_b;   // row stage: q/k/v rows, workspace store boxes
     CUtensorMap tw, tc, tqc, tout;        // column stage: workspace, c_L, q columns, output columns
+    CUtensorMap tw128, tc128;             // alpha_R stage: 128-key workspace / c_L boxes
+    CUtensorMap tar_st, tar_ld;           // hat_alpha_R [bh*gq][key][j][128]: store (32 keys), load (s2 rows)
     float* wc;                            // c_L [col][ckey_stride]
     const __nv_bfloat16* w;               // workspace W[col][part][key][64]
+    float* stats;                         // T >= 2: per (col, l) running max and 1/sum of L
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
 };
 
@@ -84,21 +87,24 @@ __host__ __device__ __forceinline__ int exchange_units(const Geometry& g) {
 
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
+#include "mbx_tc_alpha.cuh"
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 }
 
-__global__ void __launch_bounds__(kRowThreads, 1) tc_row_stage(const __grid_constant__ TcParams P, Geometry g) {
+__global__ void __launch_bounds__(kRowThreads, 1)
+tc_row_stage(const __grid_constant__ TcParams P, Geometry g, int amode, int want_y) {
     SPAN_AT(0, 0);
-    row_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr);
+    row_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr, amode != 0, want_y != 0);
     SPAN_AT(0, 1);
 }
 
-__global__ void __launch_bounds__(kColThreads, 1) tc_column_stage(const __grid_constant__ TcParams P, Geometry g) {
+__global__ void __launch_bounds__(kColThreads, 1)
+tc_column_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
     SPAN_AT(1, 0);
-    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr);
+    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr, mode);
     SPAN_AT(1, 1);
 }
 
@@ -214,7 +220,7 @@ int row_ctas_override() {
 
 bool tc_supported(const Geometry& g, int dtype, int flags) {
     if (flags & MBX_FLAG_FORCE_GENERIC) return false;
-    if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T != 1) return false;
+    if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return false;
     if (g.s2 > kMaxS2 || g.s1 > kMaxS1) return false;
     if (g.nf == 0 && (g.q_order || g.kv_order)) return false;   // rows need a closed form
     int F, H, W;
@@ -228,8 +234,10 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
 
 size_t tc_workspace_bytes(const Geometry& g) {
     const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
-    return align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4) +
-           align256((size_t)exchange_units(g) * 4);
+    size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4) +
+                   align256((size_t)exchange_units(g) * 4);
+    if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 64 * 4);   // hat_alpha_R, stats
+    return bytes;
 }
 
 cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
@@ -262,6 +270,13 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
                                                      align256((size_t)ncols * ckey_stride(g) * 4));
     P.wc = Wc;
     P.w = Wp;
+    P.stats = nullptr;
+    __nv_bfloat16* AR = nullptr;
+    if (g.T > 1) {
+        char* after = reinterpret_cast<char*>(counters) + align256((size_t)exchange_units(g) * 4);
+        AR = reinterpret_cast<__nv_bfloat16*>(after);
+        P.stats = reinterpret_cast<float*>(after + align256((size_t)rows * 256));
+    }
     {
         // blocked W[col][part][key][64]: part 0,1 = aL halves, 2,3 = Y halves
         cuuint64_t dims[4] = {64, (cuuint64_t)g.nkeys, 4, (cuuint64_t)ncols};
@@ -281,6 +296,26 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
         if (!encode(&P.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
             return cudaErrorInvalidValue;
+        if (g.T > 1) {
+            cuuint32_t box128[4] = {64, (cuuint32_t)kAKC, 1, 1};
+            if (!encode(&P.tw128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box128,
+                        CU_TENSOR_MAP_SWIZZLE_128B))
+                return cudaErrorInvalidValue;
+            cuuint32_t cbox128[2] = {(cuuint32_t)kAKC, 1};
+            if (!encode(&P.tc128, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox128,
+                        CU_TENSOR_MAP_SWIZZLE_NONE))
+                return cudaErrorInvalidValue;
+            // hat_alpha_R[bh*gq][key][j][128] bf16
+            cuuint64_t adims[4] = {128, (cuuint64_t)g.s2, (cuuint64_t)g.nkeys, (cuuint64_t)g.bh * g.gq};
+            cuuint64_t astr[3] = {256, (cuuint64_t)g.s2 * 256, (cuuint64_t)g.s2 * 256 * g.nkeys};
+            cuuint32_t abox_st[4] = {64, 1, 32, 1};
+            cuuint32_t abox_ld[4] = {64, (cuuint32_t)g.s2, 1, 1};
+            if (!encode(&P.tar_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_st,
+                        CU_TENSOR_MAP_SWIZZLE_128B) ||
+                !encode(&P.tar_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_ld,
+                        CU_TENSOR_MAP_SWIZZLE_128B))
+                return cudaErrorInvalidValue;
+        }
     }
 
     cudaError_t e;
@@ -296,7 +331,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         return e;
 
     const int sms = num_sms();
-    if (fused_enabled()) {
+    if (g.T == 1 && fused_enabled()) {
         // split of the SMs between the stages (MBX_ROW_CTAS overrides)
         int n_row = row_ctas_override();
         if (n_row <= 0) n_row = (int)(sms * 0.55);
@@ -309,17 +344,33 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         if (e == cudaSuccess) return cudaGetLastError();
         cudaGetLastError();   // not co-resident here: fall back to two launches
     }
+    const int smem_alpha = AlphaSmem::kTotal + 1024;
+    if (g.T > 1 &&
+        (e = cudaFuncSetAttribute(tc_alpha_r_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_alpha)) !=
+            cudaSuccess)
+        return e;
     const int64_t key_rows = (int64_t)g.bh * g.s1 * row_groups(g) * g.gk;   // row-stage key rows
     const int grid_row = key_rows < sms ? (int)key_rows : sms;
-    {
-        ProfScope p("tc_row_stage", stream);
-        tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(P, g);
-    }
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
     const int grid_col = ngroups < sms ? (int)ngroups : sms;
-    {
-        ProfScope p("tc_column_stage", stream);
-        tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(P, g);
+    const int64_t aitems = ncols * ((g.nkeys + kAKC - 1) / kAKC);
+    const int grid_alpha = aitems < sms ? (int)aitems : sms;
+    // refinements (solver.py:184-195): row stage (A = Q at t = 0, hat_alpha_R after), then either
+    // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1)
+    for (int t = 0; t < g.T; ++t) {
+        const int last = t == g.T - 1;
+        {
+            ProfScope p("tc_row_stage", stream);
+            tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(P, g, t > 0, last);
+        }
+        {
+            ProfScope p("tc_column_stage", stream);
+            tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(P, g, last ? 0 : 1);
+        }
+        if (!last) {
+            ProfScope p("tc_alpha_r_stage", stream);
+            tc_alpha_r_stage<<<grid_alpha, kAlphaThreads, smem_alpha, stream>>>(P, g);
+        }
     }
     return cudaGetLastError();
 }

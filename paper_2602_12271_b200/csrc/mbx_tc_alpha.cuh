@@ -1,0 +1,206 @@
+// alpha_R stage (included by mbx_tc.cu): the hand-off from refinement t to
+// t + 1 when T >= 2 (solver.py:185-186 at the next iteration):
+//     alpha_R[c,k,j,:] = sum_l L[l,(c,k)] Q[a,l,j,:],   c_R[c,k,j] = sum_l L[l,(c,k)]
+// written normalised, hat_alpha_R = alpha_R / max(c_R, eps_div) (bf16), so the next
+// row stage computes z = scale * hat_alpha_R . K exactly like the first one with Q.
+//
+// Item = (column (b,h,a,j), chunk of 128 keys).  Keys sit on the TMEM lanes:
+//   MMA1  S^T[key, l] = aL[key,:] . Q_col[l,:]          128 x 32 x 128
+//   P^T[key, l] = 2^(S^T sl2 - c_L log2e - m_l) / sum_l  (row statistics from the column
+//   stage's statistics pass), c_R = sum_l P^T -- both thread-local (one key per thread)
+//   MMA2  alpha_R[key, :] = P^T . Q_col                  128 x 128 x 64 (l padded to 64)
+//   epilogue: / max(c_R, eps) -> bf16 -> staging -> TMA store into
+//   hat_alpha_R[bh][a][key][j][128] (the next row stage's A rows).
+constexpr int kAlphaThreads = 192;   // producer, MMA, 4 x softmax / epilogue
+constexpr int kAKC = 128;            // keys per item
+struct AlphaSmem {
+    // per buffer b (2): aL [2 d-chunks][128 keys][128 B] (32 KB), Q_col [2 d-chunks][64 l][128 B]
+    // (16 KB, rows 32..63 zero), P^T [128 keys][128 B] (16 KB, l 32..63 zero), c_L [128] f32
+    static constexpr int kBuf = 65536 + 1024;           // keeps buffer 1 on a 1024 B (SW128) boundary
+    static constexpr int kA = 0, kQc = 32768, kP = 49152, kC = 65536;
+    static constexpr int kStage = 2 * kBuf;              // [4 warps][2] x [32 keys][64] bf16
+    static constexpr int kBars = kStage + 8 * 4096;
+    static constexpr int kNumBars = 10;
+    static constexpr int kTmemSlot = kBars + kNumBars * 8;
+    static constexpr int kTotal = kTmemSlot + 16;
+};
+
+__global__ void __launch_bounds__(kAlphaThreads, 1)
+tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AlphaSmem::kBars);
+    uint64_t* ld_full = bars;        // [2]
+    uint64_t* ld_empty = bars + 2;   // [2]  MMA2 done with the buffer
+    uint64_t* s_full = bars + 4;     // [2]
+    uint64_t* p_full = bars + 6;     // [2]  128 softmax threads wrote P^T, read S^T
+    uint64_t* o_full = bars + 8;     // [2]  (D2 buffer b; drained before the next s_full of b)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + AlphaSmem::kTmemSlot);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nch = (g.nkeys + kAKC - 1) / kAKC;
+    const int items = g.bh * g.gq * g.s2 * nch;
+    const int first = blockIdx.x, stride = gridDim.x;
+    const int my_items = first < items ? (items - first + stride - 1) / stride : 0;
+
+    if (tid == 0) {
+        tma_prefetch(&P.tw128);
+        tma_prefetch(&P.tc128);
+        tma_prefetch(&P.tqc);
+        tma_prefetch(&P.tar_st);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&ld_full[i], 1);
+            mbar_init(&ld_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&o_full[i], 1);
+        }
+        fence_barrier_init();
+    }
+    // zero Q_col rows 32..63 and P^T columns 32..63 once (never written afterwards)
+    for (int b = 0; b < 2; ++b) {
+        uint8_t* base = smem + b * AlphaSmem::kBuf;
+        for (int i = tid; i < 2 * 32 * 8; i += kAlphaThreads) {   // Q_col: 2 chunks x rows 32..63 x 8 x 16 B
+            const int ch = i / 256, rr = 32 + (i % 256) / 8, cc = i % 8;
+            *reinterpret_cast<uint4*>(base + AlphaSmem::kQc + ch * 8192 + rr * 128 + cc * 16) = make_uint4(0, 0, 0, 0);
+        }
+        for (int i = tid; i < 128 * 4; i += kAlphaThreads) {   // P^T: rows 0..127, logical chunks 4..7
+            const int rr = i / 4, cc = 4 + (i % 4);
+            *reinterpret_cast<uint4*>(base + AlphaSmem::kP + rr * 128 + ((cc ^ (rr & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+        }
+    }
+    if (warp == 0) tmem_alloc<512>(tmem_slot);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;   // S^T buffers at 32 b, D2 buffers at 128 + 128 b
+
+    auto decode = [&](int it, int& col, int& ch) {
+        const int item = first + it * stride;
+        ch = item % nch;
+        col = item / nch;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {   // ------------------------------------------ TMA producer
+            for (int it = 0; it < my_items; ++it) {
+                int col, ch;
+                decode(it, col, ch);
+                const int b = it & 1;
+                mbar_wait(&ld_empty[b], ((it >> 1) & 1) ^ 1);
+                uint8_t* base = smem + b * AlphaSmem::kBuf;
+                const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
+                const int64_t tok = row_base(g, true, a, 0) + j;
+                const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
+                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * 32u * 128u + kAKC * 4u);
+                tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
+                tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
+                tma_load_4d(base + AlphaSmem::kQc, &P.tqc, &ld_full[b], 0, wcol, wrow, bh);
+                tma_load_4d(base + AlphaSmem::kQc + 8192, &P.tqc, &ld_full[b], 64, wcol, wrow, bh);
+                tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ------------------------------------------ MMA issuer
+            const uint32_t id1 = idesc_bf16(128, 32, false, false);
+            const uint32_t id2 = idesc_bf16(128, 128, false, true);
+            for (int it = 0; it < my_items; ++it) {
+                const int b = it & 1;
+                mbar_wait(&ld_full[b], (it >> 1) & 1);
+                // S^T buffer b free: the softmax of item it-2 read it (p_full(it-2) precedes it)
+                if (it >= 2) mbar_wait(&p_full[b], ((it >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t base = smem_u32(smem + b * AlphaSmem::kBuf);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_bf16(tmem + b * 32,
+                             smem_desc(base + AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
+                             smem_desc(base + AlphaSmem::kQc + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2), id1,
+                             kk > 0);
+                mma_commit(&s_full[b]);
+                // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
+                // which the softmax threads finish before arriving on p_full(it))
+                mbar_wait(&p_full[b], (it >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16(tmem + 128 + b * 128, smem_desc(base + AlphaSmem::kP + kk * 32, 16, 1024, 2),
+                             smem_desc(base + AlphaSmem::kQc + kk * 2048, 8192, 1024, 2), id2, kk > 0);
+                mma_commit(&o_full[b]);
+                mma_commit(&ld_empty[b]);
+            }
+        }
+    } else if (warp < 6) {
+        // ------------------------------------------ softmax (thread = key) + epilogue
+        const int quad = warp & 3;
+        const int r = quad * 32 + lane;   // key within the chunk
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const float sl2 = g.scale * kLog2e;
+        uint8_t* stg_base = smem + AlphaSmem::kStage + quad * 8192;
+        int nstore = 0;
+        for (int it = 0; it < my_items; ++it) {
+            int col, ch;
+            decode(it, col, ch);
+            const int b = it & 1;
+            uint8_t* base = smem + b * AlphaSmem::kBuf;
+            const int key = ch * kAKC + r;
+            const bool key_ok = key < g.nkeys;
+            // row statistics of this column (written by the statistics pass)
+            const float* st = P.stats + (int64_t)col * 64;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            float x[32];
+            tmem_ld32(tmem + b * 32 + lane_off, x);
+            const float cl = reinterpret_cast<const float*>(base + AlphaSmem::kC)[r] * kLog2e;
+            float p[32], cr = 0.f;
+#pragma unroll
+            for (int l = 0; l < 32; ++l) {
+                const float e = ex2(fmaf(x[l], sl2, -cl) - __ldg(st + l)) * __ldg(st + 32 + l);
+                p[l] = (l < g.s1 && key_ok) ? e : 0.f;
+                cr += p[l];
+            }
+            // P^T row (keys on rows, l along K): logical 16-byte chunks 0..3 of the SW128 row
+            const uint32_t prow = smem_u32(base + AlphaSmem::kP) + r * 128;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc)
+                st_shared_v4(prow + ((cc ^ (r & 7)) << 4), pack_bf16(p[8 * cc], p[8 * cc + 1]),
+                             pack_bf16(p[8 * cc + 2], p[8 * cc + 3]), pack_bf16(p[8 * cc + 4], p[8 * cc + 5]),
+                             pack_bf16(p[8 * cc + 6], p[8 * cc + 7]));
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(&p_full[b]);
+            // epilogue of this item: hat_alpha_R[key, :] = D2[key, :] / max(c_R, eps)
+            mbar_wait(&o_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            const float inv = 1.f / fmaxf(cr, g.eps_div);
+            const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
+#pragma unroll 1
+            for (int part = 0; part < 2; ++part) {
+                float o[64];
+                tmem_ld32(tmem + 128 + b * 128 + lane_off + part * 64, o);
+                tmem_ld32(tmem + 128 + b * 128 + lane_off + part * 64 + 32, o + 32);
+                uint8_t* stg = stg_base + (nstore++ & 1) * 4096;
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                const uint32_t srow = smem_u32(stg) + lane * 128;
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc)
+                    st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pack_bf16(o[8 * cc] * inv, o[8 * cc + 1] * inv),
+                                 pack_bf16(o[8 * cc + 2] * inv, o[8 * cc + 3] * inv),
+                                 pack_bf16(o[8 * cc + 4] * inv, o[8 * cc + 5] * inv),
+                                 pack_bf16(o[8 * cc + 6] * inv, o[8 * cc + 7] * inv));
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && ch * kAKC + quad * 32 < g.nkeys) {   // box rows past nkeys are clipped
+                    tma_store_4d(&P.tar_st, stg, part * 64, j, ch * kAKC + quad * 32, bh * g.gq + a);
+                    bulk_commit();
+                }
+            }
+            tc_fence_before();
+        }
+        if (lane == 0) bulk_wait<0>();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}

@@ -12,6 +12,8 @@
 // 128 lanes carry value dims:
 //     MMA_O_i  O^T_i[v, l] += Y_i^T . P_i^T            M=128, N=32, K=96
 // (solver.py:192-195 joint softmax with bias -c_L; factors.py:124 O = L Y).
+// column-stage trace points are off (the trace buffer holds the row stage's roles)
+#define TRC(role, idx, tag) ((void)0)
 constexpr int kColThreads = 192;   // 6 warps: producer, MMA, 4 x softmax/output
 constexpr int kKC = 96;            // keys per chunk (S_i is 96 TMEM columns)
 constexpr int kRing = 5;           // aL / Y chunk slots
@@ -43,8 +45,11 @@ __device__ __forceinline__ void unit_wait(const unsigned* counters, int u, unsig
 
 // Column-stage role of CTA `first` among `stride` column CTAs.  counters != nullptr:
 // wait for each exchange unit before reading it and discard its L2 lines after use.
+// mode 0: O = L Y (last refinement); mode 1 (T >= 2, earlier refinements): only the
+// per-row softmax statistics (running max, sum) of L, for the alpha_R stage.
 __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
-                                         const unsigned* counters) {
+                                         const unsigned* counters, int mode = 0) {
+    const bool outm = mode == 0;
     const CUtensorMap& tm_w = P.tw;
     const CUtensorMap& tm_c = P.tc;
     const CUtensorMap& tm_qc = P.tqc;
@@ -119,7 +124,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 int bh, a, j0;
                 decode(first + gi * stride, bh, a, j0);
                 mbar_wait(q_empty, (gi & 1) ^ 1);
-                TR(8, ti, 5);
+                TRC(8, ti, 5);
                 mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
                 for (int i = 0; i < 4; ++i) {
                     const int64_t tok0 = row_base(g, true, a, 0) + j0 + i;
@@ -142,24 +147,24 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     }
                     for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
                         const int slot = n % kRing;
-                        TR(8, ti, 1);
+                        TRC(8, ti, 1);
                         mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TR(8, ti, 2);
+                        TRC(8, ti, 2);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
                         tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
                         const int cb = i * 2 + (u & 1);
                         mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
-                        TR(8, ti, 4);
+                        TRC(8, ti, 4);
                         mbar_expect_tx(&c_full[cb], kKC * 4u);
                         tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
                     }
-                    for (int i = 0; i < 4; ++i, ++n) {   // Y_i
+                    for (int i = 0; i < 4 && outm; ++i, ++n) {   // Y_i
                         const int slot = n % kRing;
-                        TR(8, ti, 6);
+                        TRC(8, ti, 6);
                         mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TR(8, ti, 7);
+                        TRC(8, ti, 7);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0 + i);
@@ -178,15 +183,15 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
             int ti = 0;
             for (int gi = 0; gi < my_groups; ++gi) {
                 mbar_wait(q_full, gi & 1);
-                TR(9, ti, 16);
+                TRC(9, ti, 16);
                 for (int ch = 0; ch < nch; ++ch) {
                     const int u = gi * nch + ch;
                     for (int i = 0; i < 4; ++i, ++n) {
                         const int slot = n % kRing;
                         mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TR(9, ti, 11);
+                        TRC(9, ti, 11);
                         if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
-                        TR(9, ti, 12);
+                        TRC(9, ti, 12);
                         tc_fence_after();
                         const uint32_t sA = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
 #pragma unroll
@@ -199,12 +204,12 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                         mma_commit(&ring_empty[slot]);
                     }
                     if (ch == nch - 1) mma_commit(q_empty);
-                    for (int i = 0; i < 4; ++i, ++n) {
+                    for (int i = 0; i < 4 && outm; ++i, ++n) {
                         const int slot = n % kRing;
                         mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TR(9, ti, 13);
+                        TRC(9, ti, 13);
                         mbar_wait(&p_full[i], u & 1);
-                        TR(9, ti, 14);
+                        TRC(9, ti, 14);
                         if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
                         tc_fence_after();
                         const uint32_t sY = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
@@ -240,9 +245,9 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 const int cb = quad * 2 + (u & 1);
                 const uint32_t cbuf = smem_u32(smem + ColSmem::kC + cb * 512);
                 mbar_wait(&c_full[cb], (u >> 1) & 1);
-                if (lane == 0) TR(warp + 8, ti, 21);
+                if (lane == 0) TRC(warp + 8, ti, 21);
                 mbar_wait(&s_full[quad], u & 1);
-                if (lane == 0) TR(warp + 8, ti, 22);
+                if (lane == 0) TRC(warp + 8, ti, 22);
                 tc_fence_after();
                 float x[kKC];
                 tmem_ld32(tmem + quad * kKC + lane_off, x);
@@ -278,6 +283,18 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     need = 1;
                 }
                 s_run *= fac;
+                if (!outm) {   // statistics only: running sum of this chunk, no P, no O
+                    float sq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int k = 0; k < kKC; k += 4) {
+                        sq[0] += ex2(x[k] - m_run);
+                        sq[1] += ex2(x[k + 1] - m_run);
+                        sq[2] += ex2(x[k + 2] - m_run);
+                        sq[3] += ex2(x[k + 3] - m_run);
+                    }
+                    s_run += (sq[0] + sq[1]) + (sq[2] + sq[3]);
+                    continue;
+                }
                 if (ch > 0) {
                     const int any = __any_sync(0xffffffffu, need);
                     stat_fac[quad * 32 + l] = fac;
@@ -320,7 +337,15 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 s_run += sum;
                 fence_proxy_async_smem();
                 mbar_arrive(&p_full[quad]);
-                if (lane == 0) TR(warp + 8, ti, 23);
+                if (lane == 0) TRC(warp + 8, ti, 23);
+            }
+            if (!outm) {   // L statistics of row l of column j0 + quad (log2 units, x = S sl2 - c_L log2e)
+                if (j0 + quad < g.s2) {
+                    const int col = (bh * g.gq + a) * g.s2 + j0 + quad;
+                    P.stats[(int64_t)col * 64 + l] = m_run;
+                    P.stats[(int64_t)col * 64 + 32 + l] = 1.f / s_run;
+                }
+                continue;
             }
             // ---- output of the 4 columns: O[l, v] = O^T_i[v, l] / s_l ----
             // tile rows are contiguous W-token grid rows: token(l, j) = row_base(a,0) + j + l*W
@@ -338,14 +363,14 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
             const int ulast = gi * nch + nch - 1;
-            if (lane == 0) TR(warp + 8, ti, 25);
+            if (lane == 0) TRC(warp + 8, ti, 25);
             for (int i = 0; i < 4; ++i) {
                 mbar_wait(&o_done[i], ulast & 1);
-                if (lane == 0) TR(warp + 8, ti, 26);
+                if (lane == 0) TRC(warp + 8, ti, 26);
                 tc_fence_after();
                 float o[32];
                 tmem_ld32(tmem + 4 * kKC + i * 32 + lane_off, o);
-                if (lane == 0) TR(warp + 8, ti, 28);
+                if (lane == 0) TRC(warp + 8, ti, 28);
                 float inv[32];
 #pragma unroll
                 for (int q4 = 0; q4 < 32; q4 += 4) {
@@ -371,7 +396,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                         bulk_commit();
                     }
                 }
-                if (lane == 0) TR(warp + 8, ti, 29);
+                if (lane == 0) TRC(warp + 8, ti, 29);
             }
             if (counters) {   // this group's workspace lines are dead: drop them from L2 unwritten
                 for (int i = 0; i < 4; ++i) {
@@ -383,7 +408,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 }
             }
             tc_fence_before();
-            if (lane == 0) TR(warp + 8, ti, 27);
+            if (lane == 0) TRC(warp + 8, ti, 27);
             mbar_arrive(o_free);
             named_sync(1, 128);   // stat_sum / rb reused by the next group
         }

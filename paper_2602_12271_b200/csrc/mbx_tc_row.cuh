@@ -24,11 +24,14 @@ struct RowSmem {
     static constexpr int kQ = 0;
     static constexpr int kQChunk = kQG * 8192;
     static constexpr int kQBytes = 2 * kQChunk;
-    static constexpr int kKV = kQBytes;               // KV[3]: [K c0 | K c1 | V c0 | V c1] 8 KB each
+    // refinements t >= 1: A ring of two [2 d-chunks][128 rows][128 B] tiles (hat_alpha_R rows) in the same region
+    static constexpr int kASlot = 32768;
+    static constexpr int kQRegion = 2 * kASlot;
+    static constexpr int kKV = kQRegion;              // KV[3]: [K c0 | K c1 | V c0 | V c1] 8 KB each
     static constexpr int kKVBytes = 32768;
     static constexpr int kStage = kKV + kKVStages * kKVBytes;   // staging [8 warps][2] x [32][64] bf16
     static constexpr int kBars = kStage + 16 * 4096;
-    static constexpr int kNumBars = 2 + 2 * kKVStages + 2 + 2 + 4;
+    static constexpr int kNumBars = 2 + 2 * kKVStages + 2 + 2 + 4 + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
@@ -141,8 +144,10 @@ __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc)
 
 // Row-stage role of CTA `first` among `stride` row CTAs.  counters == nullptr: no
 // exchange signalling (two-launch path, contiguous key-row ranges).
+// amode: MMA1's A rows come from hat_alpha_R of the previous refinement (per task,
+// smem) instead of Q (per item, TMEM); want_y: compute Y = R V (last refinement only).
 __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
-                                         unsigned* counters) {
+                                         unsigned* counters, bool amode = false, bool want_y = true) {
     const CUtensorMap& tm_q = P.tq;
     const CUtensorMap& tm_k = P.tk;
     const CUtensorMap& tm_v = P.tv;
@@ -158,6 +163,8 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
     uint64_t* p_full = s_full + 2;                // [2]
     uint64_t* o_full = p_full + 2;                // [2] O_aL / O_Y written
     uint64_t* o_empty = o_full + 2;               // [2] O_aL / O_Y drained
+    uint64_t* a_full = o_empty + 2;               // [2] amode: A tile of task landed
+    uint64_t* a_empty = a_full + 2;               // [2] amode: MMA1 done with it
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowSmem::kTmemSlot);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -183,6 +190,8 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
         for (int i = 0; i < 2; ++i) {
             mbar_init(&o_full[i], 1);
             mbar_init(&o_empty[i], 128);
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
         }
         fence_barrier_init();
     }
@@ -228,7 +237,23 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     tma_load_4d(qb + RowSmem::kQChunk + la * 8192, &tm_q, q_full, 64, tok, h, b);
                 }
             };
-            if (cur.my_items > 0) load_q(0);
+            int ta = 0;   // amode: tasks whose A tile was issued
+            // amode: A tile of task (key tile c, M tile mt) = hat_alpha_R rows j of tiles 2mt, 2mt+1
+            auto load_a = [&](int c, int mt) {
+                const int sl = ta & 1;
+                WAITX(&a_empty[sl], ((ta >> 1) & 1) ^ 1);
+                const int nla = min(2, cur.nt - 2 * mt);
+                mbar_expect_tx(&a_full[sl], 2u * box_bytes * (uint32_t)nla);
+                uint8_t* ab = smem + RowSmem::kQ + sl * RowSmem::kASlot;
+                const int key = c * g.s1 + cur.kr;
+                for (int la = 0; la < nla; ++la) {
+                    const int ag = cur.bh * g.gq + kQG * cur.qg + 2 * mt + la;
+                    tma_load_4d(ab + la * 8192, &P.tar_ld, &a_full[sl], 0, 0, key, ag);
+                    tma_load_4d(ab + 16384 + la * 8192, &P.tar_ld, &a_full[sl], 64, 0, key, ag);
+                }
+                ++ta;
+            };
+            if (cur.my_items > 0 && !amode) load_q(0);
             for (int li = 0; li < cur.my_items; ++li) {
                 cur.li = li;
                 cur.load(g);
@@ -249,7 +274,11 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
                     tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
                     tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
-                    if (c == ((P.dbg & 256) ? cur.c0 : cur.c1 - 1) && li + 1 < cur.my_items) load_q(li + 1);
+                    if (amode) {
+                        for (int mt = 0; mt < cur.n_mt; ++mt) load_a(c, mt);
+                    } else if (c == ((P.dbg & 256) ? cur.c0 : cur.c1 - 1) && li + 1 < cur.my_items) {
+                        load_q(li + 1);
+                    }
                 }
             }
         }
@@ -272,7 +301,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 bool did = false;
                 // MMA2(to): softmax done with S/P buffer to%2, both O buffers drained by task to-1
                 if (co.valid && to < ts && ((P.dbg & 32) || (mbar_test(&p_full[to & 1], (to >> 1) & 1) &&
-                    mbar_test(&o_empty[0], (to & 1) ^ 1) && mbar_test(&o_empty[1], (to & 1) ^ 1)))) {
+                    mbar_test(&o_empty[0], (to & 1) ^ 1) && (!want_y || mbar_test(&o_empty[1], (to & 1) ^ 1))))) {
                     TR(1, ti, 12);
                     tc_fence_after();
                     // B = [K | V] row, MN-major SW128 (LBO 8192 between 64-feature atoms)
@@ -280,6 +309,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     const uint32_t pa = tmem + kRowS + (to & 1) * 64;
 #pragma unroll
                     for (int s = 0; s < 2; ++s) {   // s = 0: aL = P K, s = 1: Y = P V
+                        if (s == 1 && !want_y) break;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
                             mma_bf16_ts(tmem + kRowO + s * 128, pa + kk * 8,
@@ -294,7 +324,9 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 // MMA1(ts): S/P buffer ts%2 released by MMA2(ts-2), Q of its item in TMEM, K/V landed
                 if (cs.valid && ts < to + 2) {
                     bool ready = true;
-                    if (cs.li != q_item) {
+                    if (amode) {
+                        ready = mbar_test(&a_full[ts & 1], (ts >> 1) & 1);
+                    } else if (cs.li != q_item) {
                         // first task of a new item: all MMA1 of the previous item are issued,
                         // so (tensor-pipe order) the copy cannot overtake their reads of Q
                         if (mbar_test(q_full, cs.li & 1)) {
@@ -322,10 +354,19 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                         const uint32_t b_lo = kv_lo + (uint32_t)cs.kst * (RowSmem::kKVBytes >> 4) + (1u << 16);
                         const uint32_t a_t = tmem + kRowQ + cs.mt * 64;
                         const uint32_t d_t = tmem + kRowS + (ts & 1) * 64;
+                        if (amode) {   // A = hat_alpha_R rows of this task, K-major SW128 in smem
+                            const uint32_t a_lo = q_lo + (uint32_t)(ts & 1) * (RowSmem::kASlot >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
-                            mma_bf16_ts(d_t, a_t + kk * 8, desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)),
-                                        idesc_s, kk > 0);
+                            for (int kk = 0; kk < 8; ++kk)
+                                mma_bf16(d_t, desc(a_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
+                            mma_commit(&a_empty[ts & 1]);
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk)
+                                mma_bf16_ts(d_t, a_t + kk * 8,
+                                            desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
+                        }
                         mma_commit(&s_full[ts & 1]);
                         if (cs.last_mt()) s_kv_ok = false;
                         cs.advance(g);
@@ -428,7 +469,8 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
         }
     } else {
         // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
-        const int set = warp >= 10 ? 1 : 0;   // warps 6-9: O_aL (quarters 0,1), 10-13: O_Y (2,3)
+        const int set = warp >= 10 ? 1 : 0;   // warps 6-9: O_aL, 10-13: O_Y
+        if (set == 1 && !want_y) cur.valid = false;   // no Y this refinement
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + kRowO + set * 128 + lane_off;

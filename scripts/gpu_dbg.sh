@@ -1,7 +1,5 @@
 #!/bin/bash
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/dbg_pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/dbg_pytest.log
-for d in 0 558; do
+for d in 0 1024 558; do
   echo "dbg $d $(MBX_DBG=$d timeout 300 python bench.py --steps 20 --warmup 5 --config sf --no-cpu --no-dense 2>/dev/null | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print([(k["name"], k["ms_avg"]) for k in d["kernels"]])')" >> gpurun_out/dbg.txt
 done
-MBX_DBG=558 NCTA=1 timeout 120 python scripts/trace_tc.py sf > gpurun_out/t558.txt 2>&1
 NCTA=1 timeout 120 python scripts/trace_tc.py sf > gpurun_out/t0.txt 2>&1

@@ -174,23 +174,26 @@ def test_factors_row_stochastic_on_device(cuda):
     assert (lf.sum(dim=(4, 5, 8)) - 1).abs().max().item() < 1e-5
 
 
-@pytest.mark.parametrize("frames,q_frames,B,H", [(3, 3, 1, 12), (5, 3, 2, 2), (21, 3, 1, 1)])
-def test_tensor_core_path(cuda, frames, q_frames, B, H):
-    """The tcgen05 path is the one selected for the hot shapes and matches both
-    the oracle (2e-2) and the SIMT path run on the same inputs."""
-    g = torch.Generator(device="cpu").manual_seed(frames)
+@pytest.mark.parametrize("frames,q_frames,B,H,T", [(3, 3, 1, 12, 1), (5, 3, 2, 2, 1), (21, 3, 1, 1, 1),
+                                                   (3, 3, 1, 4, 2), (3, 3, 1, 2, 3), (7, 3, 1, 2, 2),
+                                                   (21, 3, 1, 1, 3)])
+def test_tensor_core_path(cuda, frames, q_frames, B, H, T):
+    """The tcgen05 path is the one selected for the hot shapes -- for every
+    refinement count (T >= 2 adds the statistics / alpha_R hand-off kernels) --
+    and matches both the oracle (2e-2) and the SIMT path run on the same inputs."""
+    g = torch.Generator(device="cpu").manual_seed(frames * 10 + T)
     h, w = 30, 52
     q = torch.randn(B, H, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
     k = torch.randn(B, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
     v = torch.randn(B, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
     plan = _sf_plan(frames, h, w)
     low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
-    assert ops.selected_path(q, k, v, low) == "tcgen05"
-    out = ops.forward(q, k, v, low)
-    ref_simt = ops.forward(q, k, v, low, force_generic=True)
+    assert ops.selected_path(q, k, v, low, T) == "tcgen05"
+    out = ops.forward(q, k, v, low, T)
+    ref_simt = ops.forward(q, k, v, low, T, force_generic=True)
     assert orc.rel_l2(out.float().cpu().numpy(), ref_simt.float().cpu().numpy()) < 1e-2
     nh = min(H, 2)
-    ref = _oracle_heads(q[:1, :nh], k[:1, :nh], v[:1, :nh], low, 1)
+    ref = _oracle_heads(q[:1, :nh], k[:1, :nh], v[:1, :nh], low, T)
     assert orc.rel_l2(out[:1, :nh].float().cpu().numpy(), ref) < BF16_TOL
 
 
