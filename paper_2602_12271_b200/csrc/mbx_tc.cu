@@ -68,6 +68,10 @@ struct TcParams {
     float* wc;                            // c_L [col][ckey_stride]
     const __nv_bfloat16* w;               // workspace W[col][part][key][64]
     float* stats;                         // T >= 2: per (col, l) running max and 1/sum of L
+    int stats_pitch;                      // floats per column: [max x s1p | 1/sum x s1p]
+    CUtensorMap tqcw, toutw;              // wide column stage: q columns (128 rows), output rows (32 x 64)
+    __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
+    int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
 };
 
@@ -88,6 +92,7 @@ __host__ __device__ __forceinline__ int exchange_units(const Geometry& g) {
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
 #include "mbx_tc_alpha.cuh"
+#include "mbx_tc_colw.cuh"
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -221,7 +226,8 @@ int row_ctas_override() {
 bool tc_supported(const Geometry& g, int dtype, int flags) {
     if (flags & MBX_FLAG_FORCE_GENERIC) return false;
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return false;
-    if (g.s2 > kMaxS2 || g.s1 > kMaxS1) return false;
+    if (g.s2 > kMaxS2) return false;
+    if (g.T > 1 && g.s1 > kMaxS1) return false;   // alpha_R hand-off: l on the MMA N axis (<= 32)
     if (g.nf == 0 && (g.q_order || g.kv_order)) return false;   // rows need a closed form
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return false;
@@ -236,7 +242,7 @@ size_t tc_workspace_bytes(const Geometry& g) {
     const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
     size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4) +
                    align256((size_t)exchange_units(g) * 4);
-    if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 64 * 4);   // hat_alpha_R, stats
+    if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 2 * ((g.s1 + 31) / 32) * 32 * 4);
     return bytes;
 }
 
@@ -271,6 +277,22 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     P.wc = Wc;
     P.w = Wp;
     P.stats = nullptr;
+    const int s1p = ((g.s1 + 31) / 32) * 32;
+    P.stats_pitch = 2 * s1p;
+    P.out = reinterpret_cast<__nv_bfloat16*>(out);
+    P.out_bh_stride = g.os[1];
+    P.out_tok_stride = g.os[2];
+    const bool wide = g.s1 > kMaxS1;
+    if (wide) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
+        cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
+        cuuint64_t qstr[3] = {(cuuint64_t)g.qs[2] * 2, (cuuint64_t)g.qs[2] * 2 * g.W, (cuuint64_t)g.qs[1] * 2};
+        cuuint32_t qbox[4] = {64, 1, 128, 1};
+        cuuint64_t ostr[3] = {(cuuint64_t)g.os[2] * 2, (cuuint64_t)g.os[2] * 2 * g.W, (cuuint64_t)g.os[1] * 2};
+        cuuint32_t obox[4] = {64, 1, 32, 1};
+        if (!encode(&P.tqcw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !encode(&P.toutw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, ostr, obox, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+    }
     __nv_bfloat16* AR = nullptr;
     if (g.T > 1) {
         char* after = reinterpret_cast<char*>(counters) + align256((size_t)exchange_units(g) * 4);
@@ -296,7 +318,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
         if (!encode(&P.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
             return cudaErrorInvalidValue;
-        if (g.T > 1) {
+        if (g.T > 1 || wide) {
             cuuint32_t box128[4] = {64, (cuuint32_t)kAKC, 1, 1};
             if (!encode(&P.tw128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box128,
                         CU_TENSOR_MAP_SWIZZLE_128B))
@@ -305,6 +327,8 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
             if (!encode(&P.tc128, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox128,
                         CU_TENSOR_MAP_SWIZZLE_NONE))
                 return cudaErrorInvalidValue;
+        }
+        if (g.T > 1) {
             // hat_alpha_R[bh*gq][key][j][128] bf16
             cuuint64_t adims[4] = {128, (cuuint64_t)g.s2, (cuuint64_t)g.nkeys, (cuuint64_t)g.bh * g.gq};
             cuuint64_t astr[3] = {256, (cuuint64_t)g.s2 * 256, (cuuint64_t)g.s2 * 256 * g.nkeys};
@@ -331,7 +355,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         return e;
 
     const int sms = num_sms();
-    if (g.T == 1 && fused_enabled()) {
+    if (g.T == 1 && !wide && fused_enabled()) {
         // split of the SMs between the stages (MBX_ROW_CTAS overrides)
         int n_row = row_ctas_override();
         if (n_row <= 0) n_row = (int)(sms * 0.55);
@@ -345,6 +369,12 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cudaGetLastError();   // not co-resident here: fall back to two launches
     }
     const int smem_alpha = AlphaSmem::kTotal + 1024;
+    const int smem_wide = WideSmem::kTotal + 1024;
+    if (wide && (e = cudaFuncSetAttribute(tc_column_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_wide)) !=
+                    cudaSuccess)
+        return e;
+    const int64_t witems = ncols * ((g.s1 + 127) / 128);
+    const int grid_wide = witems < sms ? (int)witems : sms;
     if (g.T > 1 &&
         (e = cudaFuncSetAttribute(tc_alpha_r_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_alpha)) !=
             cudaSuccess)
@@ -363,7 +393,10 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
             ProfScope p("tc_row_stage", stream);
             tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(P, g, t > 0, last);
         }
-        {
+        if (wide) {
+            ProfScope p("tc_column_wide", stream);
+            tc_column_wide<<<grid_wide, kWideThreads, smem_wide, stream>>>(P, g, last ? 0 : 1);
+        } else {
             ProfScope p("tc_column_stage", stream);
             tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(P, g, last ? 0 : 1);
         }

@@ -146,7 +146,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             const int key = ch * kAKC + r;
             const bool key_ok = key < g.nkeys;
             // row statistics of this column (written by the statistics pass)
-            const float* st = P.stats + (int64_t)col * 64;
+            const float* st = P.stats + (int64_t)col * P.stats_pitch;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
             float x[32];
@@ -155,7 +155,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             float p[32], cr = 0.f;
 #pragma unroll
             for (int l = 0; l < 32; ++l) {
-                const float e = ex2(fmaf(x[l], sl2, -cl) - __ldg(st + l)) * __ldg(st + 32 + l);
+                const float e = ex2(fmaf(x[l], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
                 p[l] = (l < g.s1 && key_ok) ? e : 0.f;
                 cr += p[l];
             }

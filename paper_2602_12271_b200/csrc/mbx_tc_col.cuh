@@ -342,8 +342,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
             if (!outm) {   // L statistics of row l of column j0 + quad (log2 units, x = S sl2 - c_L log2e)
                 if (j0 + quad < g.s2) {
                     const int col = (bh * g.gq + a) * g.s2 + j0 + quad;
-                    P.stats[(int64_t)col * 64 + l] = m_run;
-                    P.stats[(int64_t)col * 64 + 32 + l] = 1.f / s_run;
+                    P.stats[(int64_t)col * P.stats_pitch + l] = m_run;
+                    P.stats[(int64_t)col * P.stats_pitch + P.stats_pitch / 2 + l] = 1.f / s_run;
                 }
                 continue;
             }

@@ -201,3 +201,28 @@ def test_rejects_cpu_tensors():
     q = torch.zeros(1, 1, 4680, 128)
     with pytest.raises(pk.SolverError):
         pk.monarch_attention(q, q, q, _sf_plan())
+
+
+@pytest.mark.parametrize("frames,q_frames,nb,H", [(3, 3, (3, 30, 52), 2), (6, 3, (3, 30, 52), 2),
+                                                  (2, 2, None, 2), (5, 5, (5, 30, 52), 1)])
+def test_wide_column_path(cuda, frames, q_frames, nb, H):
+    """Plans with more than 32 rows per tile -- the paper's (3h, w) tiles (s1 = 90),
+    an untiled (fh, w) config (s1 = 60) and s1 = 150 (two M tiles) -- run the row
+    stage plus the FlashAttention-style wide column stage on tensor cores."""
+    g = torch.Generator(device="cpu").manual_seed(frames * 7 + q_frames)
+    h, w = 30, 52
+    q = torch.randn(1, H, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k = torch.randn(1, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    v = torch.randn(1, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    shape = pk.VideoShape(frames, h, w)
+    if nb is None:
+        plan = pk.aligned_config(shape, ("f", "h"))
+        low = pk.lower_square(plan)
+    else:
+        plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
+        low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
+    assert low.s1 > 32
+    assert ops.selected_path(q, k, v, low) == "tcgen05"
+    out = ops.forward(q, k, v, low)
+    ref = _oracle_heads(q, k, v, low, 1)
+    assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
