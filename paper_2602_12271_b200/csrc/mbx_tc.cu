@@ -216,6 +216,10 @@ bool fused_enabled() {
     const char* e = getenv("MBX_FUSED");
     return e && e[0] == '1';
 }
+bool pdl_enabled() {   // MBX_PDL=0 disables programmatic dependent launch
+    const char* e = getenv("MBX_PDL");
+    return !(e && e[0] == '0');
+}
 int row_ctas_override() {
     const char* e = getenv("MBX_ROW_CTAS");
     return e ? atoi(e) : 0;
@@ -282,7 +286,8 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     P.out = reinterpret_cast<__nv_bfloat16*>(out);
     P.out_bh_stride = g.os[1];
     P.out_tok_stride = g.os[2];
-    const bool wide = g.s1 > kMaxS1;
+    const char* wide_env = getenv("MBX_WIDE");   // 1: FlashAttention-style column stage for any s1 (experiments)
+    const bool wide = g.s1 > kMaxS1 || (g.T == 1 && wide_env && wide_env[0] == '1');
     if (wide) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
         cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
         cuuint64_t qstr[3] = {(cuuint64_t)g.qs[2] * 2, (cuuint64_t)g.qs[2] * 2 * g.W, (cuuint64_t)g.qs[1] * 2};
@@ -385,24 +390,49 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int grid_col = ngroups < sms ? (int)ngroups : sms;
     const int64_t aitems = ncols * ((g.nkeys + kAKC - 1) / kAKC);
     const int grid_alpha = aitems < sms ? (int)aitems : sms;
+    // Every launch after the first uses programmatic dependent launch: its CTAs set up
+    // while the previous stage drains and wait (griddepcontrol.wait) before touching
+    // the workspace.  The first launch is ordinary, so it never overlaps the previous
+    // forward's readers of the workspace.
+    int nlaunch = 0;
+    auto launch = [&](const void* fn, int grid, int threads, int smem, void** args) -> cudaError_t {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = (nlaunch++ > 0 && pdl_enabled()) ? 1 : 0;
+        return cudaLaunchKernelExC(&cfg, fn, args);
+    };
     // refinements (solver.py:184-195): row stage (A = Q at t = 0, hat_alpha_R after), then either
     // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1)
     for (int t = 0; t < g.T; ++t) {
-        const int last = t == g.T - 1;
+        int last = t == g.T - 1, amode = t > 0, mode = last ? 0 : 1;
         {
             ProfScope p("tc_row_stage", stream);
-            tc_row_stage<<<grid_row, kRowThreads, smem_row, stream>>>(P, g, t > 0, last);
+            void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
+            if ((e = launch((const void*)tc_row_stage, grid_row, kRowThreads, smem_row, args)) != cudaSuccess) return e;
         }
         if (wide) {
             ProfScope p("tc_column_wide", stream);
-            tc_column_wide<<<grid_wide, kWideThreads, smem_wide, stream>>>(P, g, last ? 0 : 1);
+            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+            if ((e = launch((const void*)tc_column_wide, grid_wide, kWideThreads, smem_wide, args)) != cudaSuccess)
+                return e;
         } else {
             ProfScope p("tc_column_stage", stream);
-            tc_column_stage<<<grid_col, kColThreads, smem_col, stream>>>(P, g, last ? 0 : 1);
+            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+            if ((e = launch((const void*)tc_column_stage, grid_col, kColThreads, smem_col, args)) != cudaSuccess)
+                return e;
         }
         if (!last) {
             ProfScope p("tc_alpha_r_stage", stream);
-            tc_alpha_r_stage<<<grid_alpha, kAlphaThreads, smem_alpha, stream>>>(P, g);
+            void* args[] = {(void*)&P, (void*)&g};
+            if ((e = launch((const void*)tc_alpha_r_stage, grid_alpha, kAlphaThreads, smem_alpha, args)) != cudaSuccess)
+                return e;
         }
     }
     return cudaGetLastError();

@@ -74,6 +74,8 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;   // S^T buffers at 32 b, D2 buffers at 128 + 128 b
+    pdl_trigger();   // dependents may start their prologue once every CTA got here
+    pdl_wait();      // predecessor kernels (previous stage) complete and visible
 
     auto decode = [&](int it, int& col, int& ch) {
         const int item = first + it * stride;

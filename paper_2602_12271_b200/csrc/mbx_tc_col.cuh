@@ -107,6 +107,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();   // dependents may start their prologue once every CTA got here
+    pdl_wait();      // predecessor kernels (previous stage) complete and visible
 
     auto decode = [&](int grp, int& bh, int& a, int& j0) {
         const int jg = grp % gpt;

@@ -78,6 +78,8 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();   // dependents may start their prologue once every CTA got here
+    pdl_wait();      // predecessor kernels (previous stage) complete and visible
 
     // item -> (column col, M tile mt); column -> (bh, a, j)
     auto decode = [&](int it, int& col, int& mt) {
