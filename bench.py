@@ -45,6 +45,14 @@ CONFIGS = {
              "C3 chunked-KV rollout: 3 query frames vs 21 KV frames, (h,w)-tiled"),
     "n32k": (1, 12, 21, 21, 30, 52, 128, (1, 30, 52), "bf16",
              "C4 N=32760 (21,30,52), (h,w)-tiled G=21"),
+    "kv21_3hw": (1, 12, 21, 3, 30, 52, 128, (3, 30, 52), "bf16",
+                 "C3b chunked-KV rollout: 3 query frames vs 21 KV frames, (3h,w)-tiled (paper's s=0.97)"),
+    "n32k_3hw": (1, 12, 21, 21, 30, 52, 128, (3, 30, 52), "bf16",
+                 "C4b N=32760 (21,30,52), (3h,w)-tiled G=7 (paper's Wan 480p s=0.97)"),
+    "n32k_fhw": (1, 12, 21, 21, 30, 52, 128, None, "bf16",
+                 "C4c N=32760 untiled aligned (fh,w) = (630,52)"),
+    "n32k_mis": (1, 12, 21, 21, 30, 52, 128, "mis", "bf16",
+                 "C4d N=32760 untiled misaligned raw (b1,b2) = (1260,26)"),
     "c1": (1, 2, 1, 1, 32, 32, 64, None, "fp32",
            "C1 CPU-reference config: B=1 H=2 N=1024 (32,32) untiled fp32"),
 }
@@ -68,6 +76,9 @@ def workload(name, iterations):
     shape = pk.VideoShape(fkv, h, w)
     if nb is None:
         plan = pk.aligned_config(shape, ("f", "h"))
+        low = pk.lower_square(plan)
+    elif nb == "mis":
+        plan = pk.config_from_sizes(shape, 1260, 26)
         low = pk.lower_square(plan)
     else:
         plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)

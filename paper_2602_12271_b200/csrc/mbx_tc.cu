@@ -12,6 +12,7 @@
 
 #include <cuda.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -169,7 +170,7 @@ bool make_rows_map(CUtensorMap* m, const void* base, int B, int H, int N, const 
 bool make_outcol_map(CUtensorMap* m, const void* base, const Geometry& g, int nq) {
     cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
     cuuint64_t strides[3] = {(cuuint64_t)g.os[2] * 2, (cuuint64_t)g.os[2] * 2 * g.W, (cuuint64_t)g.os[1] * 2};
-    cuuint32_t box[4] = {32, 1, (cuuint32_t)g.s1, 1};
+    cuuint32_t box[4] = {32, 1, (cuuint32_t)(g.s1 < kMaxS1 ? g.s1 : kMaxS1), 1};   // stacked stage only (s1 <= 32)
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
@@ -231,7 +232,7 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
     if (flags & MBX_FLAG_FORCE_GENERIC) return false;
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return false;
     if (g.s2 > kMaxS2) return false;
-    if (g.T > 1 && g.s1 > kMaxS1) return false;   // alpha_R hand-off: l on the MMA N axis (<= 32)
+    if (g.T > 1 && g.s1 > 128) return false;   // alpha_R hand-off: query rows l on the MMA N axis
     if (g.nf == 0 && (g.q_order || g.kv_order)) return false;   // rows need a closed form
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return false;
@@ -250,11 +251,18 @@ size_t tc_workspace_bytes(const Geometry& g) {
     return bytes;
 }
 
+// Failure of a host-side setup step: reported on stderr when MBX_VERBOSE is set.
+static cudaError_t tc_fail(const char* what, int line) {
+    if (getenv("MBX_VERBOSE")) fprintf(stderr, "mbx tc_forward: %s failed (mbx_tc.cu:%d)\n", what, line);
+    return cudaErrorInvalidValue;
+}
+#define TC_FAIL(what) tc_fail(what, __LINE__)
+
 cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
                        void* workspace, cudaStream_t stream) {
     Geometry g = g0;
     int F, H, W;
-    if (!column_grid(g, &F, &H, &W)) return cudaErrorInvalidValue;
+    if (!column_grid(g, &F, &H, &W)) return TC_FAIL("tensor map / argument check");
     if (g.nf == 0) {   // express the identity plan as a (1, s1, s2) neighborhood grid
         g.F = F; g.H = H; g.W = W;
         g.nf = 1; g.nh = g.s1; g.nw = g.s2;
@@ -262,7 +270,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int B = g.bh / g.heads;
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
-        return cudaErrorInvalidValue;
+        return TC_FAIL("tensor map / argument check");
     TcParams P;
     {
         const char* e = getenv("MBX_DBG");
@@ -271,7 +279,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, g.s2) ||
         !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&P.tqc, q, g, nq) ||
         !make_outcol_map(&P.tout, out, g, nq))
-        return cudaErrorInvalidValue;
+        return TC_FAIL("tensor map / argument check");
     const int64_t ncols = (int64_t)g.bh * g.gq * g.s2;
     const int64_t rows = ncols * g.nkeys;
     __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(workspace);
@@ -288,7 +296,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     P.out_tok_stride = g.os[2];
     const char* wide_env = getenv("MBX_WIDE");   // 1: FlashAttention-style column stage for any s1 (experiments)
     const bool wide = g.s1 > kMaxS1 || (g.T == 1 && wide_env && wide_env[0] == '1');
-    if (wide) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
+    if (wide || g.T > 1) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
         cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
         cuuint64_t qstr[3] = {(cuuint64_t)g.qs[2] * 2, (cuuint64_t)g.qs[2] * 2 * g.W, (cuuint64_t)g.qs[1] * 2};
         cuuint32_t qbox[4] = {64, 1, 128, 1};
@@ -296,7 +304,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t obox[4] = {64, 1, 32, 1};
         if (!encode(&P.tqcw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !encode(&P.toutw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, ostr, obox, CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
+            return TC_FAIL("tensor map / argument check");
     }
     __nv_bfloat16* AR = nullptr;
     if (g.T > 1) {
@@ -310,28 +318,28 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint64_t strides[3] = {128, (cuuint64_t)g.nkeys * 128, (cuuint64_t)g.nkeys * 512};
         cuuint32_t box[4] = {64, (cuuint32_t)kKC, 1, 1};          // column stage: contiguous 12 KB
         if (!encode(&P.tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
+            return TC_FAIL("tensor map / argument check");
         // row stage: one key, the columns j of one epilogue warp (rows 0..31 and 32..s2-1)
         cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 32 ? g.s2 : 32)};
         if (!encode(&P.tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
+            return TC_FAIL("tensor map / argument check");
         cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
         if (!encode(&P.tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
+            return TC_FAIL("tensor map / argument check");
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
         if (!encode(&P.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
-            return cudaErrorInvalidValue;
+            return TC_FAIL("tensor map / argument check");
         if (g.T > 1 || wide) {
             cuuint32_t box128[4] = {64, (cuuint32_t)kAKC, 1, 1};
             if (!encode(&P.tw128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box128,
                         CU_TENSOR_MAP_SWIZZLE_128B))
-                return cudaErrorInvalidValue;
+                return TC_FAIL("tensor map / argument check");
             cuuint32_t cbox128[2] = {(cuuint32_t)kAKC, 1};
             if (!encode(&P.tc128, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox128,
                         CU_TENSOR_MAP_SWIZZLE_NONE))
-                return cudaErrorInvalidValue;
+                return TC_FAIL("tensor map / argument check");
         }
         if (g.T > 1) {
             // hat_alpha_R[bh*gq][key][j][128] bf16
@@ -343,7 +351,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
                         CU_TENSOR_MAP_SWIZZLE_128B) ||
                 !encode(&P.tar_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_ld,
                         CU_TENSOR_MAP_SWIZZLE_128B))
-                return cudaErrorInvalidValue;
+                return TC_FAIL("tensor map / argument check");
         }
     }
 
@@ -406,7 +414,11 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = (nlaunch++ > 0 && pdl_enabled()) ? 1 : 0;
-        return cudaLaunchKernelExC(&cfg, fn, args);
+        cudaError_t le = cudaLaunchKernelExC(&cfg, fn, args);
+        if (le != cudaSuccess && getenv("MBX_VERBOSE"))
+            fprintf(stderr, "mbx tc_forward: launch %d (grid %d, smem %d) failed: %s\n", nlaunch, grid, smem,
+                    cudaGetErrorString(le));
+        return le;
     };
     // refinements (solver.py:184-195): row stage (A = Q at t = 0, hat_alpha_R after), then either
     // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1)

@@ -5,25 +5,26 @@
 // row stage computes z = scale * hat_alpha_R . K exactly like the first one with Q.
 //
 // Item = (column (b,h,a,j), chunk of 128 keys).  Keys sit on the TMEM lanes:
-//   MMA1  S^T[key, l] = aL[key,:] . Q_col[l,:]          128 x 32 x 128
+//   MMA1  S^T[key, l] = aL[key,:] . Q_col[l,:]          128 x s1p x 128   (s1p = s1 rounded to 32, <= 128)
 //   P^T[key, l] = 2^(S^T sl2 - c_L log2e - m_l) / sum_l  (row statistics from the column
 //   stage's statistics pass), c_R = sum_l P^T -- both thread-local (one key per thread)
-//   MMA2  alpha_R[key, :] = P^T . Q_col                  128 x 128 x 64 (l padded to 64)
+//   MMA2  alpha_R[key, :] = P^T . Q_col                  128 x 128 x s1p
 //   epilogue: / max(c_R, eps) -> bf16 -> staging -> TMA store into
 //   hat_alpha_R[bh][a][key][j][128] (the next row stage's A rows).
 constexpr int kAlphaThreads = 192;   // producer, MMA, 4 x softmax / epilogue
 constexpr int kAKC = 128;            // keys per item
 struct AlphaSmem {
-    // per buffer b (2): aL [2 d-chunks][128 keys][128 B] (32 KB), Q_col [2 d-chunks][64 l][128 B]
-    // (16 KB, rows 32..63 zero), P^T [128 keys][128 B] (16 KB, l 32..63 zero), c_L [128] f32
-    static constexpr int kBuf = 65536 + 1024;           // keeps buffer 1 on a 1024 B (SW128) boundary
-    static constexpr int kA = 0, kQc = 32768, kP = 49152, kC = 65536;
-    static constexpr int kStage = 2 * kBuf;              // [4 warps][2] x [32 keys][64] bf16
-    static constexpr int kBars = kStage + 8 * 4096;
+    // per buffer b (2): aL [2 d-chunks][128 keys][128 B] (32 KB), Q_col [2 d-chunks][128 l][128 B]
+    // (32 KB), P^T [2 l-chunks][128 keys][128 B] (32 KB), c_L [128] f32 (1 KB slot)
+    static constexpr int kA = 0, kQc = 32768, kP = 65536, kC = 98304;
+    static constexpr int kBuf = kC + 1024;               // keeps buffer 1 on a 1024 B (SW128) boundary
+    static constexpr int kStage = 2 * kBuf;              // [4 warps] x [32 keys][64] bf16 (one slot each)
+    static constexpr int kBars = kStage + 4 * 4096;
     static constexpr int kNumBars = 10;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
+static_assert(AlphaSmem::kTotal + 1024 <= 232448, "alpha_R stage exceeds 227 KB of shared memory");
 
 __global__ void __launch_bounds__(kAlphaThreads, 1)
 tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
@@ -45,7 +46,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
     if (tid == 0) {
         tma_prefetch(&P.tw128);
         tma_prefetch(&P.tc128);
-        tma_prefetch(&P.tqc);
+        tma_prefetch(&P.tqcw);
         tma_prefetch(&P.tar_st);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&ld_full[i], 1);
@@ -56,24 +57,15 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
         }
         fence_barrier_init();
     }
-    // zero Q_col rows 32..63 and P^T columns 32..63 once (never written afterwards)
-    for (int b = 0; b < 2; ++b) {
-        uint8_t* base = smem + b * AlphaSmem::kBuf;
-        for (int i = tid; i < 2 * 32 * 8; i += kAlphaThreads) {   // Q_col: 2 chunks x rows 32..63 x 8 x 16 B
-            const int ch = i / 256, rr = 32 + (i % 256) / 8, cc = i % 8;
-            *reinterpret_cast<uint4*>(base + AlphaSmem::kQc + ch * 8192 + rr * 128 + cc * 16) = make_uint4(0, 0, 0, 0);
-        }
-        for (int i = tid; i < 128 * 4; i += kAlphaThreads) {   // P^T: rows 0..127, logical chunks 4..7
-            const int rr = i / 4, cc = 4 + (i % 4);
-            *reinterpret_cast<uint4*>(base + AlphaSmem::kP + rr * 128 + ((cc ^ (rr & 7)) << 4)) = make_uint4(0, 0, 0, 0);
-        }
-    }
+    // l padded to s1p (multiple of 32): Q_col rows >= s1 (TMA loads s1p rows: finite data or OOB
+    // zeros) meet P^T columns that are written as zeros below, so nothing needs pre-zeroing.
+    const int s1p = ((g.s1 + 31) / 32) * 32;
     if (warp == 0) tmem_alloc<512>(tmem_slot);
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;   // S^T buffers at 32 b, D2 buffers at 128 + 128 b
+    const uint32_t tmem = *tmem_slot;   // S^T buffers at 128 b, D2 buffers at 256 + 128 b
     pdl_trigger();   // dependents may start their prologue once every CTA got here
     pdl_wait();      // predecessor kernels (previous stage) complete and visible
 
@@ -94,17 +86,17 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
                 const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
                 const int64_t tok = row_base(g, true, a, 0) + j;
                 const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
-                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * 32u * 128u + kAKC * 4u);
+                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * 128u * 128u + kAKC * 4u);
                 tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
                 tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
-                tma_load_4d(base + AlphaSmem::kQc, &P.tqc, &ld_full[b], 0, wcol, wrow, bh);
-                tma_load_4d(base + AlphaSmem::kQc + 8192, &P.tqc, &ld_full[b], 64, wcol, wrow, bh);
+                tma_load_4d(base + AlphaSmem::kQc, &P.tqcw, &ld_full[b], 0, wcol, wrow, bh);
+                tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqcw, &ld_full[b], 64, wcol, wrow, bh);
                 tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {   // ------------------------------------------ MMA issuer
-            const uint32_t id1 = idesc_bf16(128, 32, false, false);
+            const uint32_t id1 = idesc_bf16(128, s1p, false, false);
             const uint32_t id2 = idesc_bf16(128, 128, false, true);
             for (int it = 0; it < my_items; ++it) {
                 const int b = it & 1;
@@ -115,19 +107,19 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
                 const uint32_t base = smem_u32(smem + b * AlphaSmem::kBuf);
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_bf16(tmem + b * 32,
+                    mma_bf16(tmem + b * 128,
                              smem_desc(base + AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
-                             smem_desc(base + AlphaSmem::kQc + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2), id1,
+                             smem_desc(base + AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2), id1,
                              kk > 0);
                 mma_commit(&s_full[b]);
                 // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
                 // which the softmax threads finish before arriving on p_full(it))
                 mbar_wait(&p_full[b], (it >> 1) & 1);
                 tc_fence_after();
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    mma_bf16(tmem + 128 + b * 128, smem_desc(base + AlphaSmem::kP + kk * 32, 16, 1024, 2),
-                             smem_desc(base + AlphaSmem::kQc + kk * 2048, 8192, 1024, 2), id2, kk > 0);
+                for (int kk = 0; kk < s1p / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
+                    mma_bf16(tmem + 256 + b * 128,
+                             smem_desc(base + AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
+                             smem_desc(base + AlphaSmem::kQc + kk * 2048, 16384, 1024, 2), id2, kk > 0);
                 mma_commit(&o_full[b]);
                 mma_commit(&ld_empty[b]);
             }
@@ -138,8 +130,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
         const int r = quad * 32 + lane;   // key within the chunk
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const float sl2 = g.scale * kLog2e;
-        uint8_t* stg_base = smem + AlphaSmem::kStage + quad * 8192;
-        int nstore = 0;
+        uint8_t* stg_base = smem + AlphaSmem::kStage + quad * 4096;
         for (int it = 0; it < my_items; ++it) {
             int col, ch;
             decode(it, col, ch);
@@ -151,23 +142,30 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             const float* st = P.stats + (int64_t)col * P.stats_pitch;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             tc_fence_after();
-            float x[32];
-            tmem_ld32(tmem + b * 32 + lane_off, x);
             const float cl = reinterpret_cast<const float*>(base + AlphaSmem::kC)[r] * kLog2e;
-            float p[32], cr = 0.f;
-#pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                const float e = ex2(fmaf(x[l], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
-                p[l] = (l < g.s1 && key_ok) ? e : 0.f;
-                cr += p[l];
-            }
-            // P^T row (keys on rows, l along K): logical 16-byte chunks 0..3 of the SW128 row
+            float cr = 0.f;
             const uint32_t prow = smem_u32(base + AlphaSmem::kP) + r * 128;
+            for (int l0 = 0; l0 < s1p; l0 += 32) {   // 32 query rows l per pass
+                float x[32];
+                tmem_ld32(tmem + b * 128 + lane_off + l0, x);
+                float p[32];
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc)
-                st_shared_v4(prow + ((cc ^ (r & 7)) << 4), pack_bf16(p[8 * cc], p[8 * cc + 1]),
-                             pack_bf16(p[8 * cc + 2], p[8 * cc + 3]), pack_bf16(p[8 * cc + 4], p[8 * cc + 5]),
-                             pack_bf16(p[8 * cc + 6], p[8 * cc + 7]));
+                for (int i = 0; i < 32; ++i) {
+                    const int l = l0 + i;
+                    const float e = ex2(fmaf(x[i], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
+                    p[i] = (l < g.s1 && key_ok) ? e : 0.f;
+                    cr += p[i];
+                }
+                // P^T row (keys on rows, l along K): 64-l chunk l0 / 64, logical 16 B chunks (l0 % 64) / 8 ..
+                const uint32_t pr = prow + (l0 >> 6) * 16384;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int lc = ((l0 & 63) >> 3) + cc;
+                    st_shared_v4(pr + ((lc ^ (r & 7)) << 4), pack_bf16(p[8 * cc], p[8 * cc + 1]),
+                                 pack_bf16(p[8 * cc + 2], p[8 * cc + 3]), pack_bf16(p[8 * cc + 4], p[8 * cc + 5]),
+                                 pack_bf16(p[8 * cc + 6], p[8 * cc + 7]));
+                }
+            }
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
@@ -179,10 +177,10 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
 #pragma unroll 1
             for (int part = 0; part < 2; ++part) {
                 float o[64];
-                tmem_ld32(tmem + 128 + b * 128 + lane_off + part * 64, o);
-                tmem_ld32(tmem + 128 + b * 128 + lane_off + part * 64 + 32, o + 32);
-                uint8_t* stg = stg_base + (nstore++ & 1) * 4096;
-                if (lane == 0) bulk_wait_read<1>();
+                tmem_ld32(tmem + 256 + b * 128 + lane_off + part * 64, o);
+                tmem_ld32(tmem + 256 + b * 128 + lane_off + part * 64 + 32, o + 32);
+                uint8_t* stg = stg_base;
+                if (lane == 0) bulk_wait_read<0>();
                 __syncwarp();
                 const uint32_t srow = smem_u32(stg) + lane * 128;
 #pragma unroll

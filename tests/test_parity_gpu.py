@@ -203,13 +203,17 @@ def test_rejects_cpu_tensors():
         pk.monarch_attention(q, q, q, _sf_plan())
 
 
-@pytest.mark.parametrize("frames,q_frames,nb,H", [(3, 3, (3, 30, 52), 2), (6, 3, (3, 30, 52), 2),
-                                                  (2, 2, None, 2), (5, 5, (5, 30, 52), 1)])
-def test_wide_column_path(cuda, frames, q_frames, nb, H):
+@pytest.mark.parametrize("frames,q_frames,nb,H,T", [(3, 3, (3, 30, 52), 2, 1), (6, 3, (3, 30, 52), 2, 1),
+                                                    (2, 2, None, 2, 1), (5, 5, (5, 30, 52), 1, 1),
+                                                    (7, 7, None, 1, 1), (5, 5, "raw", 1, 1),
+                                                    (3, 3, (3, 30, 52), 2, 2), (6, 3, (3, 30, 52), 1, 3),
+                                                    (4, 4, (4, 30, 52), 1, 2)])
+def test_wide_column_path(cuda, frames, q_frames, nb, H, T):
     """Plans with more than 32 rows per tile -- the paper's (3h, w) tiles (s1 = 90),
-    an untiled (fh, w) config (s1 = 60) and s1 = 150 (two M tiles) -- run the row
-    stage plus the FlashAttention-style wide column stage on tensor cores."""
-    g = torch.Generator(device="cpu").manual_seed(frames * 7 + q_frames)
+    untiled (fh, w) configs (s1 = 60, 210), s1 = 150 (two M tiles), a raw
+    misaligned (b1, b2) = (300, 26) blocking, and T = 2, 3 (alpha_R hand-off with
+    up to 128 query rows) -- run on tensor cores and match the oracle."""
+    g = torch.Generator(device="cpu").manual_seed(frames * 7 + q_frames + 100 * T)
     h, w = 30, 52
     q = torch.randn(1, H, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
     k = torch.randn(1, H, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
@@ -218,11 +222,14 @@ def test_wide_column_path(cuda, frames, q_frames, nb, H):
     if nb is None:
         plan = pk.aligned_config(shape, ("f", "h"))
         low = pk.lower_square(plan)
+    elif nb == "raw":
+        plan = pk.config_from_sizes(shape, 300, 26)
+        low = pk.lower_square(plan)
     else:
         plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
         low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
     assert low.s1 > 32
-    assert ops.selected_path(q, k, v, low) == "tcgen05"
-    out = ops.forward(q, k, v, low)
-    ref = _oracle_heads(q, k, v, low, 1)
+    assert ops.selected_path(q, k, v, low, T) == "tcgen05"
+    out = ops.forward(q, k, v, low, T)
+    ref = _oracle_heads(q, k, v, low, T)
     assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
