@@ -31,7 +31,7 @@ struct RowSmem {
     static constexpr int kKVBytes = 32768;
     static constexpr int kStage = kKV + kKVStages * kKVBytes;   // staging [8 warps][2] x [32][64] bf16
     static constexpr int kBars = kStage + 16 * 4096;
-    static constexpr int kNumBars = 2 + 2 * kKVStages + 2 + 2 + 4 + 4;
+    static constexpr int kNumBars = 6 + 2 * kKVStages + 2 + 2 + 4 + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
@@ -155,9 +155,9 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
     const CUtensorMap& tm_wst_b = P.tws_b;
     float* __restrict__ Wc = P.wc;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RowSmem::kBars);
-    uint64_t* q_full = bars + 0;                  // Q staging landed
-    uint64_t* q_empty = bars + 1;                 // Q staging copied into TMEM
-    uint64_t* kv_full = bars + 2;                 // [3]
+    uint64_t* q_full = bars + 0;                  // [3] Q staging slot landed
+    uint64_t* q_empty = bars + 3;                 // [3] Q staging slot copied into TMEM
+    uint64_t* kv_full = bars + 6;                 // [3]
     uint64_t* kv_empty = kv_full + kKVStages;     // [3]
     uint64_t* s_full = kv_empty + kKVStages;      // [2]
     uint64_t* p_full = s_full + 2;                // [2]
@@ -166,10 +166,16 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
     uint64_t* a_full = o_empty + 2;               // [2] amode: A tile of task landed
     uint64_t* a_empty = a_full + 2;               // [2] amode: MMA1 done with it
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowSmem::kTmemSlot);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
 
     const uint32_t box_bytes = (uint32_t)g.s2 * 128u;
     const int ckey = ckey_stride(g);
+    // Q staging: slots of [2 d-chunks][nt_max tiles][64 rows][128 B]; with one query tile per
+    // item (the (3h,w) / untiled plans) three slots let Q loads run two items ahead
+    const int nt_max = g.gq < kQG ? g.gq : kQG;
+    const int qchunk = nt_max * 8192;
+    const int nqs = kQG / nt_max;
 
     if (tid == 0) {
         tma_prefetch(&tm_q);
@@ -177,8 +183,10 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_wst);
         tma_prefetch(&tm_wst_b);
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int i = 0; i < 3; ++i) {
+            mbar_init(&q_full[i], 1);
+            mbar_init(&q_empty[i], 1);
+        }
         for (int i = 0; i < kKVStages; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
@@ -225,18 +233,19 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 qc.li = li;
                 qc.load(g);
                 const int b = qc.bh / g.heads, h = qc.bh % g.heads;
-                WAITX(q_empty, (li & 1) ^ 1);
+                const int sl = li % nqs;
+                WAITX(&q_empty[sl], ((li / nqs) & 1) ^ 1);
                 TR(0, ti, 1);
                 if ((P.dbg & 512) && li > 0) {   // timing experiment: reuse the staged Q rows
-                    mbar_arrive(q_full);
+                    mbar_arrive(&q_full[sl]);
                     return;
                 }
-                mbar_expect_tx(q_full, 2u * box_bytes * (uint32_t)qc.nt);
-                uint8_t* qb = smem + RowSmem::kQ;
+                mbar_expect_tx(&q_full[sl], 2u * box_bytes * (uint32_t)qc.nt);
+                uint8_t* qb = smem + RowSmem::kQ + sl * 2 * qchunk;
                 for (int la = 0; la < qc.nt; ++la) {
                     const int tok = (int)row_base(g, true, kQG * qc.qg + la, qc.kr);
-                    tma_load_4d(qb + la * 8192, &tm_q, q_full, 0, tok, h, b);
-                    tma_load_4d(qb + RowSmem::kQChunk + la * 8192, &tm_q, q_full, 64, tok, h, b);
+                    tma_load_4d(qb + la * 8192, &tm_q, &q_full[sl], 0, tok, h, b);
+                    tma_load_4d(qb + qchunk + la * 8192, &tm_q, &q_full[sl], 64, tok, h, b);
                 }
             };
             int ta = 0;   // amode: tasks whose A tile was issued
@@ -255,18 +264,26 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 }
                 ++ta;
             };
-            if (cur.my_items > 0 && !amode) load_q(0);
+            // Q loads are issued whenever a staging slot is free, interleaved with the K/V
+            // waits (never blocking a K/V load behind a Q slot)
+            int q_next = amode ? cur.my_items : 0;
+            auto try_q = [&]() {
+                while (q_next < cur.my_items &&
+                       mbar_test(&q_empty[q_next % nqs], (((q_next / nqs) & 1) ^ 1))) load_q(q_next++);
+            };
+            try_q();
             for (int li = 0; li < cur.my_items; ++li) {
                 cur.li = li;
                 cur.load(g);
                 const int b = cur.bh / g.heads, h = cur.bh % g.heads;
                 for (int c = cur.c0; c < cur.c1; ++c, ++kvi) {
                     const int ks = kvi % kKVStages;
-                    WAITX(&kv_empty[ks], ring_parity(kvi, kKVStages) ^ 1);
+                    const uint32_t kpar = ring_parity(kvi, kKVStages) ^ 1;
+                    while (!mbar_test(&kv_empty[ks], kpar)) try_q();
                     TR(0, ti, 2);
                     if ((P.dbg & 8) && kvi >= kKVStages) {   // timing experiment: reuse resident K/V
                         mbar_arrive(&kv_full[ks]);
-                        if (c == cur.c1 - 1 && li + 1 < cur.my_items) load_q(li + 1);
+                        try_q();
                         continue;
                     }
                     mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
@@ -276,19 +293,20 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
                     tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
                     tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
-                    if (amode) {
+                    if (amode)
                         for (int mt = 0; mt < cur.n_mt; ++mt) load_a(c, mt);
-                    } else if (c == ((P.dbg & 256) ? cur.c0 : cur.c1 - 1) && li + 1 < cur.my_items) {
-                        load_q(li + 1);
-                    }
+                    try_q();
                 }
             }
+            while (q_next < cur.my_items) load_q(q_next++);   // (blocking) remaining Q rows
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer (readiness order)
-        // The single issuing thread is on the critical path: descriptors are precomputed
+        // The whole warp runs the loop on warp-uniform state (so descriptors live in uniform
+        // registers) and one elected lane issues the tcgen05 ops; descriptors are precomputed
         // (only the 14-bit start-address field moves) and ring positions kept incrementally.
-        if (lane == 0) {
+        {
+            const bool leader = elect_one();
             const uint32_t idesc_s = idesc_bf16(128, 64, false, false);
             const uint32_t idesc_o = idesc_bf16(128, 128, false, true);
             constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
@@ -302,23 +320,26 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
             while (cs.valid || co.valid) {
                 bool did = false;
                 // MMA2(to): softmax done with S/P buffer to%2, both O buffers drained by task to-1
-                if (co.valid && to < ts && ((P.dbg & 32) || (mbar_test(&p_full[to & 1], (to >> 1) & 1) &&
-                    mbar_test(&o_empty[0], (to & 1) ^ 1) && (!want_y || mbar_test(&o_empty[1], (to & 1) ^ 1))))) {
-                    TR(1, ti, 12);
+                if (co.valid && to < ts && ((P.dbg & 32) || (mbar_test_uniform(&p_full[to & 1], (to >> 1) & 1) &&
+                    mbar_test_uniform(&o_empty[0], (to & 1) ^ 1) && (!want_y || mbar_test_uniform(&o_empty[1], (to & 1) ^ 1))))) {
+                    if (leader) TR(1, ti, 12);
                     tc_fence_after();
                     // B = [K | V] row, MN-major SW128 (LBO 8192 between 64-feature atoms)
                     const uint32_t b_lo = kv_lo + (uint32_t)co.kst * (RowSmem::kKVBytes >> 4) + (8192u >> 4 << 16);
                     const uint32_t pa = tmem + kRowS + (to & 1) * 64;
+                    if (leader) {
 #pragma unroll
-                    for (int s = 0; s < 2; ++s) {   // s = 0: aL = P K, s = 1: Y = P V
-                        if (s == 1 && !want_y) break;
+                        for (int s = 0; s < 2; ++s) {   // s = 0: aL = P K, s = 1: Y = P V
+                            if (s == 1 && !want_y) break;
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            mma_bf16_ts(tmem + kRowO + s * 128, pa + kk * 8,
-                                        desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), idesc_o, kk > 0);
-                        mma_commit(&o_full[s]);
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_bf16_ts(tmem + kRowO + s * 128, pa + kk * 8,
+                                            desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), idesc_o, kk > 0);
+                            mma_commit(&o_full[s]);
+                        }
+                        if (co.last_mt()) mma_commit(&kv_empty[co.kst]);
                     }
-                    if (co.last_mt()) mma_commit(&kv_empty[co.kst]);
+                    __syncwarp();
                     co.advance(g);
                     ++to;
                     did = true;
@@ -327,49 +348,57 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 if (cs.valid && ts < to + 2) {
                     bool ready = true;
                     if (amode) {
-                        ready = mbar_test(&a_full[ts & 1], (ts >> 1) & 1);
+                        ready = mbar_test_uniform(&a_full[ts & 1], (ts >> 1) & 1);
                     } else if (cs.li != q_item) {
                         // first task of a new item: all MMA1 of the previous item are issued,
                         // so (tensor-pipe order) the copy cannot overtake their reads of Q
-                        if (mbar_test(q_full, cs.li & 1)) {
+                        const int qsl = cs.li % nqs;
+                        if (mbar_test_uniform(&q_full[qsl], (cs.li / nqs) & 1)) {
                             tc_fence_after();
-                            for (int mt = 0; mt < cs.n_mt; ++mt)
+                            if (leader) {
+                                for (int mt = 0; mt < cs.n_mt; ++mt)
 #pragma unroll
-                                for (int kk = 0; kk < 8; ++kk)
-                                    tmem_cp_128x256b(tmem + kRowQ + mt * 64 + kk * 8,
-                                                     desc(q_lo + (((kk >> 2) * RowSmem::kQChunk + mt * 16384 +
-                                                                   (kk & 3) * 32) >> 4)));
-                            mma_commit(q_empty);
+                                    for (int kk = 0; kk < 8; ++kk)
+                                        tmem_cp_128x256b(tmem + kRowQ + mt * 64 + kk * 8,
+                                                         desc(q_lo + ((qsl * 2 * qchunk + (kk >> 2) * qchunk +
+                                                                       mt * 16384 + (kk & 3) * 32) >> 4)));
+                                mma_commit(&q_empty[qsl]);
+                            }
+                            __syncwarp();
                             q_item = cs.li;
                         } else {
                             ready = false;
                         }
                     }
                     if (ready && cs.mt == 0 && !s_kv_ok) {
-                        s_kv_ok = mbar_test(&kv_full[cs.kst], cs.kph);
+                        s_kv_ok = mbar_test_uniform(&kv_full[cs.kst], cs.kph);
                         ready = s_kv_ok;
                     }
                     if (ready) {
-                        TR(1, ti, 11);
+                        if (leader) TR(1, ti, 11);
                         tc_fence_after();
                         // B = K row, K-major SW128 (LBO 16)
                         const uint32_t b_lo = kv_lo + (uint32_t)cs.kst * (RowSmem::kKVBytes >> 4) + (1u << 16);
                         const uint32_t a_t = tmem + kRowQ + cs.mt * 64;
                         const uint32_t d_t = tmem + kRowS + (ts & 1) * 64;
-                        if (amode) {   // A = hat_alpha_R rows of this task, K-major SW128 in smem
-                            const uint32_t a_lo = q_lo + (uint32_t)(ts & 1) * (RowSmem::kASlot >> 4);
+                        if (leader) {
+                            if (amode) {   // A = hat_alpha_R rows of this task, K-major SW128 in smem
+                                const uint32_t a_lo = q_lo + (uint32_t)(ts & 1) * (RowSmem::kASlot >> 4);
 #pragma unroll
-                            for (int kk = 0; kk < 8; ++kk)
-                                mma_bf16(d_t, desc(a_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
-                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
-                            mma_commit(&a_empty[ts & 1]);
-                        } else {
+                                for (int kk = 0; kk < 8; ++kk)
+                                    mma_bf16(d_t, desc(a_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                             desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
+                                mma_commit(&a_empty[ts & 1]);
+                            } else {
 #pragma unroll
-                            for (int kk = 0; kk < 8; ++kk)
-                                mma_bf16_ts(d_t, a_t + kk * 8,
-                                            desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
+                                for (int kk = 0; kk < 8; ++kk)
+                                    mma_bf16_ts(d_t, a_t + kk * 8,
+                                                desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), idesc_s,
+                                                kk > 0);
+                            }
+                            mma_commit(&s_full[ts & 1]);
                         }
-                        mma_commit(&s_full[ts & 1]);
+                        __syncwarp();
                         if (cs.last_mt()) s_kv_ok = false;
                         cs.advance(g);
                         ++ts;

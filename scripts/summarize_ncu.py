@@ -25,7 +25,8 @@ METRICS = [
 
 
 def short(name):
-    for k in ("tc_row_stage", "tc_column_stage", "row_stage", "column_stage", "alpha_r_stage"):
+    for k in ("tc_row_stage", "tc_column_stage", "tc_column_wide", "tc_alpha_r_stage", "tc_fused", "row_stage",
+              "column_stage", "alpha_r_stage"):
         if k in name:
             return ("tc_" if name.find("tc_") >= 0 and not k.startswith("tc_") else "") + k
     return name[:60]

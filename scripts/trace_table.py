@@ -10,24 +10,24 @@ for i, ln in enumerate(lines):
     if m:
         role = int(m.group(1))
         ev[role] = [(int(t), float(x)) for t, x in re.findall(r"(\d+)@([\d.]+)", lines[i + 1])]
-mma1 = [x for t, x in ev.get(0, []) if t == 11]
-mma2 = [x for t, x in ev.get(0, []) if t == 12]
+mma1 = [x for t, x in ev.get(1, []) if t == 11]
+mma2 = [x for t, x in ev.get(1, []) if t == 12]
 sm = {}
-for role in (1,):   # softmax warp (quad 1, half 0)
+for role in (2,):   # softmax warp (quad 2)
     if role in ev:
         st = [x for t, x in ev[role] if t == 21]
         en = [x for t, x in ev[role] if t == 22]
         for k, (a, b) in enumerate(zip(st, en)):
             sm[k] = (a, b)
 epA = {}
-for role in (9,):
+for role in (6,):
     if role in ev:
         st = [x for t, x in ev[role] if t == 31]
         en = [x for t, x in ev[role] if t == 32]
         for k, (a, b) in enumerate(zip(st, en)):
             epA[k] = (a, b)
 epB = {}
-for role in (13,):
+for role in (10,):
     if role in ev:
         st = [x for t, x in ev[role] if t == 31]
         en = [x for t, x in ev[role] if t == 32]

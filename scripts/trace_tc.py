@@ -33,6 +33,8 @@ span = span.reshape(2, 256, 2).astype(np.int64)
 t0s = span[0, :, 0][span[0, :, 0] > 0].min()
 for kern, name in ((0, "row"), (1, "col")):
     ok = span[kern, :, 0] > 0
+    if not ok.any():
+        continue
     st = (span[kern, ok, 0] - t0s) / 1000.0
     en = (span[kern, ok, 1] - t0s) / 1000.0
     print(f"span {name}: ctas {ok.sum()} start min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f} "
