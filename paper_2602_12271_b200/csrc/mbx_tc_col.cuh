@@ -71,7 +71,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
     int* flags = reinterpret_cast<int*>(stat_fac + 128);                 // [4]
     int64_t* rb = reinterpret_cast<int64_t*>(flags + 4);                 // [32] row_base(a, l)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ColSmem::kTmemSlot);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
 
     const int gpt = (g.s2 + 3) >> 2;                       // column groups per query tile
     const int groups = g.bh * g.gq * gpt;
@@ -177,54 +178,64 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         }
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            const uint32_t idesc_s = idesc_bf16(128, kKC, false, false);
-            const uint32_t idesc_o = idesc_bf16(128, 32, true, false);
-            const uint32_t sQ = smem_u32(smem + ColSmem::kQ);
-            uint32_t n = 0;
-            int ti = 0;
-            for (int gi = 0; gi < my_groups; ++gi) {
-                mbar_wait(q_full, gi & 1);
-                TRC(9, ti, 16);
-                for (int ch = 0; ch < nch; ++ch) {
-                    const int u = gi * nch + ch;
-                    for (int i = 0; i < 4; ++i, ++n) {
-                        const int slot = n % kRing;
-                        mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TRC(9, ti, 11);
-                        if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
-                        TRC(9, ti, 12);
-                        tc_fence_after();
-                        const uint32_t sA = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
+        // whole warp on warp-uniform state (descriptors in uniform registers), one elected lane issues
+        const bool leader = elect_one();
+        const uint32_t idesc_s = idesc_bf16(128, kKC, false, false);
+        const uint32_t idesc_o = idesc_bf16(128, 32, true, false);
+        constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
+        auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
+        const uint32_t q_lo = ((smem_u32(smem + ColSmem::kQ) & 0x3FFFF) >> 4) | (1u << 16);
+        const uint32_t ring_lo = (smem_u32(smem + ColSmem::kRingOff) & 0x3FFFF) >> 4;
+        const uint32_t p_lo = ((smem_u32(smem + ColSmem::kP) & 0x3FFFF) >> 4) | (1u << 16);
+        int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
+        auto next_slot = [&]() {
+            if (++slot == kRing) {
+                slot = 0;
+                sph ^= 1;
+            }
+        };
+        for (int gi = 0; gi < my_groups; ++gi) {
+            mbar_wait(q_full, gi & 1);
+            for (int ch = 0; ch < nch; ++ch) {
+                const int u = gi * nch + ch;
+                for (int i = 0; i < 4; ++i) {
+                    mbar_wait(&ring_full[slot], sph);
+                    if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
+                    tc_fence_after();
+                    if (leader) {
+                        const uint32_t a_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + (1u << 16);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk) {
-                            const uint64_t ad = smem_desc(sQ + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2);
-                            const uint64_t bd = smem_desc(sA + (kk >> 2) * (kKC * 128) + (kk & 3) * 32, 16, 1024, 2);
-                            mma_bf16(tmem + i * kKC, ad, bd, idesc_s, kk > 0);
-                        }
+                        for (int kk = 0; kk < 8; ++kk)
+                            mma_bf16(tmem + i * kKC, desc(q_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                     desc(a_lo + (((kk >> 2) * (kKC * 128) + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
                         mma_commit(&s_full[i]);
                         mma_commit(&ring_empty[slot]);
                     }
-                    if (ch == nch - 1) mma_commit(q_empty);
-                    for (int i = 0; i < 4 && outm; ++i, ++n) {
-                        const int slot = n % kRing;
-                        mbar_wait(&ring_full[slot], (n / kRing) & 1);
-                        TRC(9, ti, 13);
-                        mbar_wait(&p_full[i], u & 1);
-                        TRC(9, ti, 14);
-                        if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
-                        tc_fence_after();
-                        const uint32_t sY = smem_u32(smem + ColSmem::kRingOff + slot * ColSmem::kSlot);
-                        const uint32_t sP = smem_u32(smem + ColSmem::kP + i * 8192);
+                    __syncwarp();
+                    next_slot();
+                }
+                if (ch == nch - 1) {
+                    if (leader) mma_commit(q_empty);
+                    __syncwarp();
+                }
+                for (int i = 0; i < 4 && outm; ++i) {
+                    mbar_wait(&ring_full[slot], sph);
+                    mbar_wait(&p_full[i], u & 1);
+                    if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
+                    tc_fence_after();
+                    if (leader) {
+                        // A = Y^T (MN-major, LBO kKC*128 between the two 64-value halves), B = P_i (K-major)
+                        const uint32_t y_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + ((kKC * 128) >> 4 << 16);
+                        const uint32_t pb = p_lo + (uint32_t)i * (8192 >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < kKC / 16; ++kk) {
-                            const uint64_t ad = smem_desc(sY + kk * 2048, kKC * 128, 1024, 2);
-                            const uint64_t bd = smem_desc(sP + (kk >> 2) * 4096 + (kk & 3) * 32, 16, 1024, 2);
-                            mma_bf16(tmem + 4 * kKC + i * 32, ad, bd, idesc_o, ch > 0 || kk > 0);
-                        }
+                        for (int kk = 0; kk < kKC / 16; ++kk)
+                            mma_bf16(tmem + 4 * kKC + i * 32, desc(y_lo + ((kk * 2048) >> 4)),
+                                     desc(pb + (((kk >> 2) * 4096 + (kk & 3) * 32) >> 4)), idesc_o, ch > 0 || kk > 0);
                         mma_commit(&ring_empty[slot]);
                         mma_commit(&o_done[i]);
                     }
+                    __syncwarp();
+                    next_slot();
                 }
             }
         }

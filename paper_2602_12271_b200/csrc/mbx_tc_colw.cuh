@@ -43,7 +43,8 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
                                       //     two chunks, so a wait can never be two phases behind)
     uint64_t* o_free = bars + 22;     // (128) O rows read out after an item
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + WideSmem::kTmemSlot);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
     const bool outm = mode == 0;
     const int n_mt = (g.s1 + 127) / 128;
     const int nch = (g.nkeys + kWKC - 1) / kWKC;
@@ -122,48 +123,59 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {   // ------------------------------------------ MMA issuer
-            const uint32_t id_s = idesc_bf16(128, kWKC, false, false);
-            const uint32_t id_o = idesc_bf16(128, 128, false, true);
-            uint32_t n = 0;
-            int u = 0;
-            for (int it = 0; it < my_items; ++it) {
-                const int qb = it & 1;
-                mbar_wait(&q_full[qb], (it >> 1) & 1);
-                const uint32_t sq = smem_u32(smem + WideSmem::kQ + qb * 32768);
-                for (int ch = 0; ch < nch; ++ch, ++u) {
-                    const int sb = u & 1;
-                    // S buffer sb free: the softmax read S(u-2) before arriving p_full(u-2)
-                    if (u >= 2) mbar_wait(&p_full[sb], ((u >> 1) - 1) & 1);
-                    const int sl = n & 3;
-                    mbar_wait(&r_full[sl], (n >> 2) & 1);
-                    tc_fence_after();
-                    const uint32_t sa = smem_u32(smem + WideSmem::kRing + sl * 32768);
+        // ------------------------------------------ MMA issuer: whole warp on warp-uniform
+        // state (descriptors in uniform registers), one elected lane issues
+        const bool leader = elect_one();
+        const uint32_t id_s = idesc_bf16(128, kWKC, false, false);
+        const uint32_t id_o = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
+        auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
+        const uint32_t q_lo = ((smem_u32(smem + WideSmem::kQ) & 0x3FFFF) >> 4) | (1u << 16);
+        const uint32_t ring_lo = (smem_u32(smem + WideSmem::kRing) & 0x3FFFF) >> 4;
+        uint32_t n = 0;
+        int u = 0;
+        for (int it = 0; it < my_items; ++it) {
+            const int qb = it & 1;
+            mbar_wait(&q_full[qb], (it >> 1) & 1);
+            const uint32_t sq = q_lo + (uint32_t)qb * (32768 >> 4);
+            for (int ch = 0; ch < nch; ++ch, ++u) {
+                const int sb = u & 1;
+                // S buffer sb free: the softmax read S(u-2) before arriving p_full(u-2)
+                if (u >= 2) mbar_wait(&p_full[sb], ((u >> 1) - 1) & 1);
+                const int sl = n & 3;
+                mbar_wait(&r_full[sl], (n >> 2) & 1);
+                tc_fence_after();
+                if (leader) {
+                    const uint32_t sa = ring_lo + (uint32_t)sl * (32768 >> 4) + (1u << 16);
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)
-                        mma_bf16(tmem + kWS + sb * 128, smem_desc(sq + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
-                                 smem_desc(sa + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2), id_s, kk > 0);
+                        mma_bf16(tmem + kWS + sb * 128, desc(sq + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                 desc(sa + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)), id_s, kk > 0);
                     mma_commit(&s_full[sb]);
                     mma_commit(&r_empty[sl]);
-                    ++n;
                     if (ch == nch - 1) mma_commit(&q_empty[qb]);
-                    if (!outm) continue;
-                    // MMA_O(u): P(u) in TMEM, Y chunk landed; the first chunk of an item
-                    // overwrites O, which the previous item's epilogue must have read
-                    mbar_wait(&p_full[sb], (u >> 1) & 1);
-                    if (ch == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);
-                    const int yl = n & 3;
-                    mbar_wait(&r_full[yl], (n >> 2) & 1);
-                    tc_fence_after();
-                    const uint32_t sy = smem_u32(smem + WideSmem::kRing + yl * 32768);
+                }
+                __syncwarp();
+                ++n;
+                if (!outm) continue;
+                // MMA_O(u): P(u) in TMEM, Y chunk landed; the first chunk of an item
+                // overwrites O, which the previous item's epilogue must have read
+                mbar_wait(&p_full[sb], (u >> 1) & 1);
+                if (ch == 0 && it > 0) mbar_wait(o_free, (it - 1) & 1);
+                const int yl = n & 3;
+                mbar_wait(&r_full[yl], (n >> 2) & 1);
+                tc_fence_after();
+                if (leader) {
+                    const uint32_t sy = ring_lo + (uint32_t)yl * (32768 >> 4) + (16384u >> 4 << 16);
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk)   // K = keys 16 kk .. 16 kk + 15; B = Y MN-major (v atoms 16 KB apart)
-                        mma_bf16_ts(tmem + kWO, tmem + kWP + sb * 64 + kk * 8,
-                                    smem_desc(sy + kk * 2048, 16384, 1024, 2), id_o, ch > 0 || kk > 0);
+                        mma_bf16_ts(tmem + kWO, tmem + kWP + sb * 64 + kk * 8, desc(sy + ((kk * 2048) >> 4)), id_o,
+                                    ch > 0 || kk > 0);
                     mma_commit(&r_empty[yl]);
                     mma_commit(&o_done[sb]);
-                    ++n;
                 }
+                __syncwarp();
+                ++n;
             }
         }
     } else if (warp < 6) {

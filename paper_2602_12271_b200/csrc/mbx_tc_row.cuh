@@ -107,7 +107,27 @@ struct RowCursor {
         }
         if (++c < c1) return;
         ++li;
-        load(g);
+        if (stride) {
+            load(g);
+            return;
+        }
+        // range schedule: items are consecutive, so decode incrementally (no divisions on
+        // the issue path): item = ((bh * n_qg + qg) * n_cc + cc) * s1 + kr with n_cc = 1
+        valid = li < my_items;
+        if (!valid) return;
+        if (++kr == g.s1) {
+            kr = 0;
+            ++unit;
+            if (++qg == n_qg) {
+                qg = 0;
+                ++bh;
+            }
+            nt = min(kQG, g.gq - kQG * qg);
+            n_mt = (nt + 1) >> 1;
+        }
+        c0 = 0;
+        c1 = li == my_items - 1 ? (L1 - 1) % cpi + 1 : g.gk;
+        c = 0;
     }
 };
 
