@@ -37,7 +37,8 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
     uint64_t* p_full = bars + 6;     // [2]  128 softmax threads wrote P^T, read S^T
     uint64_t* o_full = bars + 8;     // [2]  (D2 buffer b; drained before the next s_full of b)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + AlphaSmem::kTmemSlot);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
     const int nch = (g.nkeys + kAKC - 1) / kAKC;
     const int items = g.bh * g.gq * g.s2 * nch;
     const int first = blockIdx.x, stride = gridDim.x;
@@ -76,16 +77,18 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
     };
 
     if (warp == 0) {
-        if (lane == 0) {   // ------------------------------------------ TMA producer
-            for (int it = 0; it < my_items; ++it) {
-                int col, ch;
-                decode(it, col, ch);
-                const int b = it & 1;
-                mbar_wait(&ld_empty[b], ((it >> 1) & 1) ^ 1);
+        // ------------------------------------------ TMA producer (whole warp, elected lane issues)
+        const bool leader = elect_one();
+        for (int it = 0; it < my_items; ++it) {
+            int col, ch;
+            decode(it, col, ch);
+            const int b = it & 1;
+            mbar_wait(&ld_empty[b], ((it >> 1) & 1) ^ 1);
+            const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
+            const int64_t tok = row_base(g, true, a, 0) + j;
+            const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
+            if (leader) {
                 uint8_t* base = smem + b * AlphaSmem::kBuf;
-                const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
-                const int64_t tok = row_base(g, true, a, 0) + j;
-                const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
                 mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * 128u * 128u + kAKC * 4u);
                 tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
                 tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
@@ -93,36 +96,45 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
                 tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqcw, &ld_full[b], 64, wcol, wrow, bh);
                 tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
             }
+            __syncwarp();
         }
     } else if (warp == 1) {
-        if (lane == 0) {   // ------------------------------------------ MMA issuer
-            const uint32_t id1 = idesc_bf16(128, s1p, false, false);
-            const uint32_t id2 = idesc_bf16(128, 128, false, true);
-            for (int it = 0; it < my_items; ++it) {
-                const int b = it & 1;
-                mbar_wait(&ld_full[b], (it >> 1) & 1);
-                // S^T buffer b free: the softmax of item it-2 read it (p_full(it-2) precedes it)
-                if (it >= 2) mbar_wait(&p_full[b], ((it >> 1) - 1) & 1);
-                tc_fence_after();
-                const uint32_t base = smem_u32(smem + b * AlphaSmem::kBuf);
+        // ------------------------------------------ MMA issuer (whole warp, uniform descriptors)
+        const bool leader = elect_one();
+        const uint32_t id1 = idesc_bf16(128, s1p, false, false);
+        const uint32_t id2 = idesc_bf16(128, 128, false, true);
+        constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
+        auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
+        const uint32_t base_lo = (smem_u32(smem) & 0x3FFFF) >> 4;
+        for (int it = 0; it < my_items; ++it) {
+            const int b = it & 1;
+            mbar_wait(&ld_full[b], (it >> 1) & 1);
+            // S^T buffer b free: the softmax of item it-2 read it (p_full(it-2) precedes it)
+            if (it >= 2) mbar_wait(&p_full[b], ((it >> 1) - 1) & 1);
+            tc_fence_after();
+            const uint32_t lo = base_lo + (uint32_t)b * (AlphaSmem::kBuf >> 4);
+            if (leader) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk)
-                    mma_bf16(tmem + b * 128,
-                             smem_desc(base + AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
-                             smem_desc(base + AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2), id1,
+                    mma_bf16(tmem + b * 128, desc(lo + ((AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                             desc(lo + ((AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)), id1,
                              kk > 0);
                 mma_commit(&s_full[b]);
-                // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
-                // which the softmax threads finish before arriving on p_full(it))
-                mbar_wait(&p_full[b], (it >> 1) & 1);
-                tc_fence_after();
+            }
+            __syncwarp();
+            // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
+            // which the softmax threads finish before arriving on p_full(it))
+            mbar_wait(&p_full[b], (it >> 1) & 1);
+            tc_fence_after();
+            if (leader) {
                 for (int kk = 0; kk < s1p / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
                     mma_bf16(tmem + 256 + b * 128,
-                             smem_desc(base + AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
-                             smem_desc(base + AlphaSmem::kQc + kk * 2048, 16384, 1024, 2), id2, kk > 0);
+                             desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                             desc(lo + ((AlphaSmem::kQc + kk * 2048) >> 4) + (16384u >> 4 << 16)), id2, kk > 0);
                 mma_commit(&o_full[b]);
                 mma_commit(&ld_empty[b]);
             }
+            __syncwarp();
         }
     } else if (warp < 6) {
         // ------------------------------------------ softmax (thread = key) + epilogue

@@ -120,59 +120,64 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            uint32_t n = 0;
-            int ti = 0;
-            for (int gi = 0; gi < my_groups; ++gi) {
-                int bh, a, j0;
-                decode(first + gi * stride, bh, a, j0);
-                mbar_wait(q_empty, (gi & 1) ^ 1);
-                TRC(8, ti, 5);
+        // whole warp on warp-uniform state (TMA coordinates in uniform registers), one elected lane issues
+        const bool leader = elect_one();
+        int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
+        for (int gi = 0; gi < my_groups; ++gi) {
+            int bh, a, j0;
+            decode(first + gi * stride, bh, a, j0);
+            mbar_wait(q_empty, (gi & 1) ^ 1);
+            const int64_t tq0 = row_base(g, true, a, 0) + j0;
+            if (leader) {
                 mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
                 for (int i = 0; i < 4; ++i) {
-                    const int64_t tok0 = row_base(g, true, a, 0) + j0 + i;
+                    const int64_t tok0 = tq0 + i;
                     const int wcol = (int)(tok0 % g.W), wrow = (int)(tok0 / g.W);
                     uint8_t* dst = smem + ColSmem::kQ + i * 4096;
                     tma_load_4d(dst, &tm_qc, q_full, 0, wcol, wrow, bh);
                     tma_load_4d(dst + 16384, &tm_qc, q_full, 64, wcol, wrow, bh);
                 }
-                const int col0 = (bh * g.gq + a) * g.s2 + j0;
-                int cc_done = -1;
-                for (int ch = 0; ch < nch; ++ch) {
-                    const int u = gi * nch + ch;
-                    const int k0 = ch * kKC;
-                    if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
-                        const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
-                        const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
-                        const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
+            }
+            __syncwarp();
+            const int col0 = (bh * g.gq + a) * g.s2 + j0;
+            int cc_done = -1;
+            for (int ch = 0; ch < nch; ++ch) {
+                const int u = gi * nch + ch;
+                const int k0 = ch * kKC;
+                if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
+                    const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
+                    const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
+                    const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
+                    if (leader)
                         for (int cc = cc_done + 1; cc <= cc_hi; ++cc) unit_wait(counters, ubase + cc, unit_signals(g));
-                        cc_done = cc_hi;
-                    }
-                    for (int i = 0; i < 4; ++i, ++n) {   // aL_i + c_L_i
-                        const int slot = n % kRing;
-                        TRC(8, ti, 1);
-                        mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TRC(8, ti, 2);
+                    __syncwarp();
+                    cc_done = cc_hi;
+                }
+                for (int i = 0; i < 4; ++i) {   // aL_i + c_L_i
+                    mbar_wait(&ring_empty[slot], sph ^ 1);
+                    const int cb = i * 2 + (u & 1);
+                    mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
+                    if (leader) {
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
                         tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
-                        const int cb = i * 2 + (u & 1);
-                        mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
-                        TRC(8, ti, 4);
                         mbar_expect_tx(&c_full[cb], kKC * 4u);
                         tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
                     }
-                    for (int i = 0; i < 4 && outm; ++i, ++n) {   // Y_i
-                        const int slot = n % kRing;
-                        TRC(8, ti, 6);
-                        mbar_wait(&ring_empty[slot], ((n / kRing) & 1) ^ 1);
-                        TRC(8, ti, 7);
+                    __syncwarp();
+                    if (++slot == kRing) { slot = 0; sph ^= 1; }
+                }
+                for (int i = 0; i < 4 && outm; ++i) {   // Y_i
+                    mbar_wait(&ring_empty[slot], sph ^ 1);
+                    if (leader) {
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0 + i);
                         tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 3, col0 + i);
                     }
+                    __syncwarp();
+                    if (++slot == kRing) { slot = 0; sph ^= 1; }
                 }
             }
         }

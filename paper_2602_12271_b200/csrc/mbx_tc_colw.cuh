@@ -90,36 +90,45 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
     };
 
     if (warp == 0) {
-        if (lane == 0) {   // ------------------------------------------ TMA producer
-            uint32_t n = 0;   // ring uses
-            int u = 0;        // chunks
-            for (int it = 0; it < my_items; ++it) {
-                int col, mt;
-                decode(it, col, mt);
-                const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
-                const int64_t tok = row_base(g, true, a, 0) + j + (int64_t)mt * 128 * g.W;
-                const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
-                const int qb = it & 1;
-                mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+        // ------------------------------------------ TMA producer (whole warp, elected lane issues)
+        const bool leader = elect_one();
+        uint32_t n = 0;   // ring uses
+        int u = 0;        // chunks
+        for (int it = 0; it < my_items; ++it) {
+            int col, mt;
+            decode(it, col, mt);
+            const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
+            const int64_t tok = row_base(g, true, a, 0) + j + (int64_t)mt * 128 * g.W;
+            const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
+            const int qb = it & 1;
+            mbar_wait(&q_empty[qb], ((it >> 1) & 1) ^ 1);
+            if (leader) {
                 mbar_expect_tx(&q_full[qb], 2u * 128u * 128u);
                 uint8_t* qd = smem + WideSmem::kQ + qb * 32768;
                 tma_load_4d(qd, &P.tqcw, &q_full[qb], 0, wcol, wrow, bh);
                 tma_load_4d(qd + 16384, &P.tqcw, &q_full[qb], 64, wcol, wrow, bh);
-                for (int ch = 0; ch < nch; ++ch, ++u) {
-                    const int k0 = ch * kWKC;
-                    for (int part = 0; part < (outm ? 2 : 1); ++part, ++n) {   // aL, then Y
-                        const int sl = n & 3;
-                        mbar_wait(&r_empty[sl], ((n >> 2) & 1) ^ 1);
+            }
+            __syncwarp();
+            for (int ch = 0; ch < nch; ++ch, ++u) {
+                const int k0 = ch * kWKC;
+                for (int part = 0; part < (outm ? 2 : 1); ++part, ++n) {   // aL, then Y
+                    const int sl = n & 3;
+                    mbar_wait(&r_empty[sl], ((n >> 2) & 1) ^ 1);
+                    if (leader) {
                         mbar_expect_tx(&r_full[sl], 2u * kWKC * 128u);
                         uint8_t* dst = smem + WideSmem::kRing + sl * 32768;
                         tma_load_4d(dst, &P.tw128, &r_full[sl], 0, k0, 2 * part, col);
                         tma_load_4d(dst + 16384, &P.tw128, &r_full[sl], 0, k0, 2 * part + 1, col);
                     }
-                    const int cb = u & 1;
-                    mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
+                    __syncwarp();
+                }
+                const int cb = u & 1;
+                mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
+                if (leader) {
                     mbar_expect_tx(&c_full[cb], kWKC * 4u);
                     tma_load_2d(smem + WideSmem::kC + cb * 512, &P.tc128, &c_full[cb], k0, col);
                 }
+                __syncwarp();
             }
         }
     } else if (warp == 1) {

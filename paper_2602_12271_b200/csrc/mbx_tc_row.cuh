@@ -245,7 +245,10 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
-        if (lane == 0) {
+        // whole warp on warp-uniform state (TMA coordinates in uniform registers), the
+        // elected lane issues
+        {
+            const bool leader = elect_one();
             int ti = 0, kvi = 0;
             // Q rows of item li into the staging tile (free once the previous item's Q was copied)
             auto load_q = [&](int li) {
@@ -255,18 +258,17 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 const int b = qc.bh / g.heads, h = qc.bh % g.heads;
                 const int sl = li % nqs;
                 WAITX(&q_empty[sl], ((li / nqs) & 1) ^ 1);
-                TR(0, ti, 1);
-                if ((P.dbg & 512) && li > 0) {   // timing experiment: reuse the staged Q rows
-                    mbar_arrive(&q_full[sl]);
-                    return;
+                if (leader) {
+                    TR(0, ti, 1);
+                    mbar_expect_tx(&q_full[sl], 2u * box_bytes * (uint32_t)qc.nt);
+                    uint8_t* qb = smem + RowSmem::kQ + sl * 2 * qchunk;
+                    for (int la = 0; la < qc.nt; ++la) {
+                        const int tok = (int)row_base(g, true, kQG * qc.qg + la, qc.kr);
+                        tma_load_4d(qb + la * 8192, &tm_q, &q_full[sl], 0, tok, h, b);
+                        tma_load_4d(qb + qchunk + la * 8192, &tm_q, &q_full[sl], 64, tok, h, b);
+                    }
                 }
-                mbar_expect_tx(&q_full[sl], 2u * box_bytes * (uint32_t)qc.nt);
-                uint8_t* qb = smem + RowSmem::kQ + sl * 2 * qchunk;
-                for (int la = 0; la < qc.nt; ++la) {
-                    const int tok = (int)row_base(g, true, kQG * qc.qg + la, qc.kr);
-                    tma_load_4d(qb + la * 8192, &tm_q, &q_full[sl], 0, tok, h, b);
-                    tma_load_4d(qb + qchunk + la * 8192, &tm_q, &q_full[sl], 64, tok, h, b);
-                }
+                __syncwarp();
             };
             int ta = 0;   // amode: tasks whose A tile was issued
             // amode: A tile of task (key tile c, M tile mt) = hat_alpha_R rows j of tiles 2mt, 2mt+1
@@ -274,14 +276,17 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 const int sl = ta & 1;
                 WAITX(&a_empty[sl], ((ta >> 1) & 1) ^ 1);
                 const int nla = min(2, cur.nt - 2 * mt);
-                mbar_expect_tx(&a_full[sl], 2u * box_bytes * (uint32_t)nla);
-                uint8_t* ab = smem + RowSmem::kQ + sl * RowSmem::kASlot;
-                const int key = c * g.s1 + cur.kr;
-                for (int la = 0; la < nla; ++la) {
-                    const int ag = cur.bh * g.gq + kQG * cur.qg + 2 * mt + la;
-                    tma_load_4d(ab + la * 8192, &P.tar_ld, &a_full[sl], 0, 0, key, ag);
-                    tma_load_4d(ab + 16384 + la * 8192, &P.tar_ld, &a_full[sl], 64, 0, key, ag);
+                if (leader) {
+                    mbar_expect_tx(&a_full[sl], 2u * box_bytes * (uint32_t)nla);
+                    uint8_t* ab = smem + RowSmem::kQ + sl * RowSmem::kASlot;
+                    const int key = c * g.s1 + cur.kr;
+                    for (int la = 0; la < nla; ++la) {
+                        const int ag = cur.bh * g.gq + kQG * cur.qg + 2 * mt + la;
+                        tma_load_4d(ab + la * 8192, &P.tar_ld, &a_full[sl], 0, 0, key, ag);
+                        tma_load_4d(ab + 16384 + la * 8192, &P.tar_ld, &a_full[sl], 64, 0, key, ag);
+                    }
                 }
+                __syncwarp();
                 ++ta;
             };
             // Q loads are issued whenever a staging slot is free, interleaved with the K/V
@@ -289,7 +294,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
             int q_next = amode ? cur.my_items : 0;
             auto try_q = [&]() {
                 while (q_next < cur.my_items &&
-                       mbar_test(&q_empty[q_next % nqs], (((q_next / nqs) & 1) ^ 1))) load_q(q_next++);
+                       mbar_test_uniform(&q_empty[q_next % nqs], (((q_next / nqs) & 1) ^ 1))) load_q(q_next++);
             };
             try_q();
             for (int li = 0; li < cur.my_items; ++li) {
@@ -299,20 +304,18 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 for (int c = cur.c0; c < cur.c1; ++c, ++kvi) {
                     const int ks = kvi % kKVStages;
                     const uint32_t kpar = ring_parity(kvi, kKVStages) ^ 1;
-                    while (!mbar_test(&kv_empty[ks], kpar)) try_q();
-                    TR(0, ti, 2);
-                    if ((P.dbg & 8) && kvi >= kKVStages) {   // timing experiment: reuse resident K/V
-                        mbar_arrive(&kv_full[ks]);
-                        try_q();
-                        continue;
-                    }
-                    mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
-                    uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
+                    while (!mbar_test_uniform(&kv_empty[ks], kpar)) try_q();
                     const int tok = (int)row_base(g, false, c, cur.kr);
-                    tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
-                    tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
-                    tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
-                    tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                    if (leader) {
+                        TR(0, ti, 2);
+                        mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
+                        uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
+                        tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
+                        tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
+                        tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
+                        tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                    }
+                    __syncwarp();
                     if (amode)
                         for (int mt = 0; mt < cur.n_mt; ++mt) load_a(c, mt);
                     try_q();
