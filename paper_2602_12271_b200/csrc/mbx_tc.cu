@@ -43,6 +43,16 @@ __device__ __forceinline__ void trace_ev(int role, int& idx, int tag) {
     }
 }
 #define TR(role, idx, tag) trace_ev(role, idx, tag)
+// column-stage events (separate buffer: the row stage owns g_trace)
+__device__ unsigned long long g_trace_col[kTraceCtas][kTraceRoles][kTraceEvents];
+__device__ __forceinline__ void trace_col(int role, int& idx, int tag) {
+    if (blockIdx.x < kTraceCtas && idx < kTraceEvents) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_trace_col[blockIdx.x][role][idx++] = (t << 8) | (unsigned)tag;
+    }
+}
+#define TRC(role, idx, tag) trace_col(role, idx, tag)
 // Start / end timestamps of every CTA of the last launch of each kernel: [kernel][cta][2].
 constexpr int kSpanCtas = 256;
 __device__ unsigned long long g_span[2][kSpanCtas][2];
@@ -55,6 +65,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     do { if (threadIdx.x == 0 && blockIdx.x < kSpanCtas) g_span[kern][blockIdx.x][which] = gtimer(); } while (0)
 #else
 #define TR(role, idx, tag) ((void)0)
+#define TRC(role, idx, tag) ((void)0)
 #define SPAN_AT(kern, which) ((void)0)
 #endif
 #define SPAN_BEGIN() SPAN_AT(0, 0)
@@ -461,6 +472,14 @@ extern "C" int mbx_trace_dump(void* host, size_t bytes) {
     static unsigned long long zeros[4 * 16 * 2048];
     cudaMemcpyToSymbol(mbx::g_trace, zeros, sizeof(zeros));
     return (int)sizeof(mbx::g_trace);
+}
+extern "C" int mbx_trace_col_dump(void* host, size_t bytes) {
+    if (bytes < sizeof(mbx::g_trace_col)) return -1;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(host, mbx::g_trace_col, sizeof(mbx::g_trace_col));
+    static unsigned long long zeros[4 * 16 * 2048];
+    cudaMemcpyToSymbol(mbx::g_trace_col, zeros, sizeof(zeros));
+    return (int)sizeof(mbx::g_trace_col);
 }
 extern "C" int mbx_span_dump(void* host, size_t bytes) {
     if (bytes < sizeof(mbx::g_span)) return -1;

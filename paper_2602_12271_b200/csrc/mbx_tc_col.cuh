@@ -12,8 +12,6 @@
 // 128 lanes carry value dims:
 //     MMA_O_i  O^T_i[v, l] += Y_i^T . P_i^T            M=128, N=32, K=96
 // (solver.py:192-195 joint softmax with bias -c_L; factors.py:124 O = L Y).
-// column-stage trace points are off (the trace buffer holds the row stage's roles)
-#define TRC(role, idx, tag) ((void)0)
 constexpr int kColThreads = 192;   // 6 warps: producer, MMA, 4 x softmax/output
 constexpr int kKC = 96;            // keys per chunk (S_i is 96 TMEM columns)
 constexpr int kRing = 5;           // aL / Y chunk slots
@@ -123,10 +121,12 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         // whole warp on warp-uniform state (TMA coordinates in uniform registers), one elected lane issues
         const bool leader = elect_one();
         int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
+        int ti = 0;
         for (int gi = 0; gi < my_groups; ++gi) {
             int bh, a, j0;
             decode(first + gi * stride, bh, a, j0);
             mbar_wait(q_empty, (gi & 1) ^ 1);
+            if (leader) TRC(0, ti, 5);
             const int64_t tq0 = row_base(g, true, a, 0) + j0;
             if (leader) {
                 mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
@@ -158,6 +158,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     const int cb = i * 2 + (u & 1);
                     mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
                     if (leader) {
+                        TRC(0, ti, 1);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
@@ -171,6 +172,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 for (int i = 0; i < 4 && outm; ++i) {   // Y_i
                     mbar_wait(&ring_empty[slot], sph ^ 1);
                     if (leader) {
+                        TRC(0, ti, 2);
                         mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                         uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
                         tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0 + i);
@@ -192,6 +194,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         const uint32_t q_lo = ((smem_u32(smem + ColSmem::kQ) & 0x3FFFF) >> 4) | (1u << 16);
         const uint32_t ring_lo = (smem_u32(smem + ColSmem::kRingOff) & 0x3FFFF) >> 4;
         const uint32_t p_lo = ((smem_u32(smem + ColSmem::kP) & 0x3FFFF) >> 4) | (1u << 16);
+        int ti = 0;
         int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
         auto next_slot = [&]() {
             if (++slot == kRing) {
@@ -208,6 +211,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
                     tc_fence_after();
                     if (leader) {
+                        TRC(1, ti, 11);
                         const uint32_t a_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + (1u << 16);
 #pragma unroll
                         for (int kk = 0; kk < 8; ++kk)
@@ -229,6 +233,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
                     tc_fence_after();
                     if (leader) {
+                        TRC(1, ti, 13);
                         // A = Y^T (MN-major, LBO kKC*128 between the two 64-value halves), B = P_i (K-major)
                         const uint32_t y_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + ((kKC * 128) >> 4 << 16);
                         const uint32_t pb = p_lo + (uint32_t)i * (8192 >> 4);

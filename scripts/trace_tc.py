@@ -21,10 +21,13 @@ v = torch.randn(wl["B"], wl["H"], wl["nk"], wl["dv"], device=dev, dtype=torch.bf
 lib = _lib.load()
 lib.mbx_trace_dump.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 buf = np.zeros(4 * 16 * 2048, dtype=np.uint64)
+lib.mbx_trace_col_dump.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+bufc = np.zeros(4 * 16 * 2048, dtype=np.uint64)
 for it in range(3):
     ops.forward(q, k, v, wl["low"], 1)
     torch.cuda.synchronize()
     lib.mbx_trace_dump(buf.ctypes.data, buf.nbytes)   # keep only the last run's trace
+    lib.mbx_trace_col_dump(bufc.ctypes.data, bufc.nbytes)
 ev = buf.reshape(4, 16, 2048)
 lib.mbx_span_dump.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 span = np.zeros(2 * 256 * 2, dtype=np.uint64)
@@ -49,3 +52,15 @@ for cta in range(int(os.environ.get("NCTA", "1"))):
             continue
         print(f"cta {cta} role {role}: {len(xs)} events")
         print("  " + " ".join(f"{tag}@{(t - t0) / 1000:.2f}" for t, tag in xs[:160]))
+
+evc = bufc.reshape(4, 16, 2048)
+for cta in range(int(os.environ.get("NCTA", "1"))):
+    allt = [int(x) >> 8 for x in evc[cta].ravel() if x]
+    if not allt:
+        continue
+    for role in range(16):
+        xs = [(int(x) >> 8, int(x) & 255) for x in evc[cta, role] if x]
+        if not xs:
+            continue
+        print(f"col cta {cta} role {role}: {len(xs)} events")
+        print("  " + " ".join(f"{tag}@{(t - t0s) / 1000:.2f}" for t, tag in xs[:200]))
