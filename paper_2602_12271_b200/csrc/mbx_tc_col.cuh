@@ -122,67 +122,86 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         const bool leader = elect_one();
         int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
         int ti = 0;
-        for (int gi = 0; gi < my_groups; ++gi) {
-            int bh, a, j0;
-            decode(first + gi * stride, bh, a, j0);
-            mbar_wait(q_empty, (gi & 1) ^ 1);
-            if (leader) TRC(0, ti, 5);
-            const int64_t tq0 = row_base(g, true, a, 0) + j0;
-            if (leader) {
-                mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
-                for (int i = 0; i < 4; ++i) {
-                    const int64_t tok0 = tq0 + i;
-                    const int wcol = (int)(tok0 % g.W), wrow = (int)(tok0 / g.W);
-                    uint8_t* dst = smem + ColSmem::kQ + i * 4096;
-                    tma_load_4d(dst, &tm_qc, q_full, 0, wcol, wrow, bh);
-                    tma_load_4d(dst + 16384, &tm_qc, q_full, 64, wcol, wrow, bh);
-                }
+        auto next_slot = [&]() {
+            if (++slot == kRing) {
+                slot = 0;
+                sph ^= 1;
             }
-            __syncwarp();
-            const int col0 = (bh * g.gq + a) * g.s2 + j0;
-            int cc_done = -1;
-            for (int ch = 0; ch < nch; ++ch) {
-                const int u = gi * nch + ch;
-                const int k0 = ch * kKC;
-                if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
-                    const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
-                    const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
-                    const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
-                    if (leader)
-                        for (int cc = cc_done + 1; cc <= cc_hi; ++cc) unit_wait(counters, ubase + cc, unit_signals(g));
-                    __syncwarp();
-                    cc_done = cc_hi;
+        };
+        // Ring order = MMA order: aL(u) [+ Q at a group start], then Y(u-1) -- the aL of the next
+        // chunk is in flight while the current chunk's softmax runs (u = global chunk index)
+        const int U = my_groups * nch;
+        // one-chunk lookahead only pays with several chunks per group (MBX_DBG 2048 / 4096 force off / on)
+        const bool look = (nch > 1 || (P.dbg & 4096)) && !(P.dbg & 2048);
+        int bh = 0, a = 0, j0 = 0, col0 = 0, cc_done = -1;
+        auto load_y = [&](int up) {   // Y_i of chunk up (its group's columns col0p .. +3)
+            int bhp, ap, j0p;
+            decode(first + (up / nch) * stride, bhp, ap, j0p);
+            const int col0p = (bhp * g.gq + ap) * g.s2 + j0p, k0 = (up % nch) * kKC;
+            for (int i = 0; i < 4; ++i) {
+                mbar_wait(&ring_empty[slot], sph ^ 1);
+                if (leader) {
+                    TRC(0, ti, 2);
+                    mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
+                    uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
+                    tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0p + i);
+                    tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 3, col0p + i);
                 }
-                for (int i = 0; i < 4; ++i) {   // aL_i + c_L_i
-                    mbar_wait(&ring_empty[slot], sph ^ 1);
-                    const int cb = i * 2 + (u & 1);
-                    mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
-                    if (leader) {
-                        TRC(0, ti, 1);
-                        mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
-                        uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
-                        tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
-                        tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
-                        mbar_expect_tx(&c_full[cb], kKC * 4u);
-                        tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
-                    }
-                    __syncwarp();
-                    if (++slot == kRing) { slot = 0; sph ^= 1; }
-                }
-                for (int i = 0; i < 4 && outm; ++i) {   // Y_i
-                    mbar_wait(&ring_empty[slot], sph ^ 1);
-                    if (leader) {
-                        TRC(0, ti, 2);
-                        mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
-                        uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
-                        tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0 + i);
-                        tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 3, col0 + i);
-                    }
-                    __syncwarp();
-                    if (++slot == kRing) { slot = 0; sph ^= 1; }
-                }
+                __syncwarp();
+                next_slot();
             }
+        };
+        for (int u = 0; u < U; ++u) {
+            const int gi = u / nch, ch = u - gi * nch;
+            if (ch == 0) {
+                decode(first + gi * stride, bh, a, j0);
+                col0 = (bh * g.gq + a) * g.s2 + j0;
+                cc_done = -1;
+                mbar_wait(q_empty, (gi & 1) ^ 1);
+                if (leader) TRC(0, ti, 5);
+                const int64_t tq0 = row_base(g, true, a, 0) + j0;
+                if (leader) {
+                    mbar_expect_tx(q_full, 4u * 2u * 32u * 128u);
+                    for (int i = 0; i < 4; ++i) {
+                        const int64_t tok0 = tq0 + i;
+                        const int wcol = (int)(tok0 % g.W), wrow = (int)(tok0 / g.W);
+                        uint8_t* dst = smem + ColSmem::kQ + i * 4096;
+                        tma_load_4d(dst, &tm_qc, q_full, 0, wcol, wrow, bh);
+                        tma_load_4d(dst + 16384, &tm_qc, q_full, 64, wcol, wrow, bh);
+                    }
+                }
+                __syncwarp();
+            }
+            const int k0 = ch * kKC;
+            if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
+                const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
+                const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
+                const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
+                if (leader)
+                    for (int cc = cc_done + 1; cc <= cc_hi; ++cc) unit_wait(counters, ubase + cc, unit_signals(g));
+                __syncwarp();
+                cc_done = cc_hi;
+            }
+            for (int i = 0; i < 4; ++i) {   // aL_i + c_L_i
+                mbar_wait(&ring_empty[slot], sph ^ 1);
+                const int cb = i * 2 + (u & 1);
+                mbar_wait(&c_empty[cb], ((u >> 1) & 1) ^ 1);
+                if (leader) {
+                    TRC(0, ti, 1);
+                    mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
+                    uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
+                    tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
+                    tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
+                    mbar_expect_tx(&c_full[cb], kKC * 4u);
+                    tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
+                }
+                __syncwarp();
+                next_slot();
+            }
+            if (outm && look && u > 0) load_y(u - 1);
+            if (outm && !look) load_y(u);
         }
+        if (outm && look && U > 0) load_y(U - 1);
     } else if (warp == 1) {
         // ------------------------------------------------------ MMA issuer
         // whole warp on warp-uniform state (descriptors in uniform registers), one elected lane issues
@@ -202,53 +221,61 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 sph ^= 1;
             }
         };
-        for (int gi = 0; gi < my_groups; ++gi) {
-            mbar_wait(q_full, gi & 1);
-            for (int ch = 0; ch < nch; ++ch) {
-                const int u = gi * nch + ch;
-                for (int i = 0; i < 4; ++i) {
-                    mbar_wait(&ring_full[slot], sph);
-                    if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
-                    tc_fence_after();
-                    if (leader) {
-                        TRC(1, ti, 11);
-                        const uint32_t a_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + (1u << 16);
+        // order: S(0), then S(u), O(u-1) for u = 1 .. U-1, then O(U-1) -- the next chunk's
+        // S MMAs are queued before this chunk's O MMAs, matching the producer's ring order
+        const int U = my_groups * nch;
+        const bool look = (nch > 1 || (P.dbg & 4096)) && !(P.dbg & 2048);
+        auto issue_o = [&](int up) {
+            const int gp = up / nch, cp = up - gp * nch;
+            for (int i = 0; i < 4; ++i) {
+                mbar_wait(&ring_full[slot], sph);
+                mbar_wait(&p_full[i], up & 1);
+                if (cp == 0 && gp > 0 && i == 0) mbar_wait(o_free, (gp - 1) & 1);
+                tc_fence_after();
+                if (leader) {
+                    TRC(1, ti, 13);
+                    // A = Y^T (MN-major, LBO kKC*128 between the two 64-value halves), B = P_i (K-major)
+                    const uint32_t y_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + ((kKC * 128) >> 4 << 16);
+                    const uint32_t pb = p_lo + (uint32_t)i * (8192 >> 4);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
-                            mma_bf16(tmem + i * kKC, desc(q_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
-                                     desc(a_lo + (((kk >> 2) * (kKC * 128) + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
-                        mma_commit(&s_full[i]);
-                        mma_commit(&ring_empty[slot]);
-                    }
-                    __syncwarp();
-                    next_slot();
+                    for (int kk = 0; kk < kKC / 16; ++kk)
+                        mma_bf16(tmem + 4 * kKC + i * 32, desc(y_lo + ((kk * 2048) >> 4)),
+                                 desc(pb + (((kk >> 2) * 4096 + (kk & 3) * 32) >> 4)), idesc_o, cp > 0 || kk > 0);
+                    mma_commit(&ring_empty[slot]);
+                    mma_commit(&o_done[i]);
                 }
-                if (ch == nch - 1) {
-                    if (leader) mma_commit(q_empty);
-                    __syncwarp();
-                }
-                for (int i = 0; i < 4 && outm; ++i) {
-                    mbar_wait(&ring_full[slot], sph);
-                    mbar_wait(&p_full[i], u & 1);
-                    if (ch == 0 && gi > 0 && i == 0) mbar_wait(o_free, (gi - 1) & 1);
-                    tc_fence_after();
-                    if (leader) {
-                        TRC(1, ti, 13);
-                        // A = Y^T (MN-major, LBO kKC*128 between the two 64-value halves), B = P_i (K-major)
-                        const uint32_t y_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + ((kKC * 128) >> 4 << 16);
-                        const uint32_t pb = p_lo + (uint32_t)i * (8192 >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < kKC / 16; ++kk)
-                            mma_bf16(tmem + 4 * kKC + i * 32, desc(y_lo + ((kk * 2048) >> 4)),
-                                     desc(pb + (((kk >> 2) * 4096 + (kk & 3) * 32) >> 4)), idesc_o, ch > 0 || kk > 0);
-                        mma_commit(&ring_empty[slot]);
-                        mma_commit(&o_done[i]);
-                    }
-                    __syncwarp();
-                    next_slot();
-                }
+                __syncwarp();
+                next_slot();
             }
+        };
+        for (int u = 0; u < U; ++u) {
+            const int gi = u / nch, ch = u - gi * nch;
+            if (ch == 0) mbar_wait(q_full, gi & 1);
+            for (int i = 0; i < 4; ++i) {
+                mbar_wait(&ring_full[slot], sph);
+                if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
+                tc_fence_after();
+                if (leader) {
+                    TRC(1, ti, 11);
+                    const uint32_t a_lo = ring_lo + (uint32_t)slot * (ColSmem::kSlot >> 4) + (1u << 16);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_bf16(tmem + i * kKC, desc(q_lo + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                 desc(a_lo + (((kk >> 2) * (kKC * 128) + (kk & 3) * 32) >> 4)), idesc_s, kk > 0);
+                    mma_commit(&s_full[i]);
+                    mma_commit(&ring_empty[slot]);
+                }
+                __syncwarp();
+                next_slot();
+            }
+            if (ch == nch - 1) {
+                if (leader) mma_commit(q_empty);
+                __syncwarp();
+            }
+            if (outm && look && u > 0) issue_o(u - 1);
+            if (outm && !look) issue_o(u);
         }
+        if (outm && look && U > 0) issue_o(U - 1);
     } else if (warp < 6) {
         // ------------------------------------------------------ softmax (warp i = column i) + output
         const int quad = warp & 3;                       // column i within the group == lane quadrant
