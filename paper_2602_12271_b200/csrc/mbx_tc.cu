@@ -82,6 +82,7 @@ struct TcParams {
     float* stats;                         // T >= 2: per (col, l) running max and 1/sum of L
     int stats_pitch;                      // floats per column: [max x s1p | 1/sum x s1p]
     CUtensorMap tqcw, toutw;              // wide column stage: q columns (128 rows), output rows (32 x 64)
+    CUtensorMap tws16, tws16r;            // paired row stage: workspace stores of 16 / (s2 % 16) columns
     __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
@@ -105,6 +106,7 @@ __host__ __device__ __forceinline__ int exchange_units(const Geometry& g) {
 #include "mbx_tc_col.cuh"
 #include "mbx_tc_alpha.cuh"
 #include "mbx_tc_colw.cuh"
+#include "mbx_tc_rowp.cuh"
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -337,6 +339,12 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
         if (!encode(&P.tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
             return TC_FAIL("tensor map / argument check");
+        cuuint32_t sbox16[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 16 ? g.s2 : 16)};
+        cuuint32_t sbox16r[4] = {64, 1, 1, (cuuint32_t)(g.s2 % 16 ? g.s2 % 16 : 16)};
+        if (!encode(&P.tws16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox16, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !encode(&P.tws16r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox16r,
+                    CU_TENSOR_MAP_SWIZZLE_128B))
+            return TC_FAIL("tensor map / argument check");
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
@@ -405,6 +413,20 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         return e;
     const int64_t key_rows = (int64_t)g.bh * g.s1 * row_groups(g) * g.gk;   // row-stage key rows
     const int grid_row = key_rows < sms ? (int)key_rows : sms;
+    // half-packed row stage (two M=64 (query tile, row) halves per 128-lane task).  MBX_PAIR=0
+    // selects the classic stage (whole query tiles per M=128 task), MBX_PAIR=1 the packed one.  Packing pays when whole
+    // query tiles leave M=128 lanes idle (odd G_q); for G_q > 1 a K/V row then serves halves
+    // of two items, so it is re-read once more -- cheap only while K and V sit in L2.
+    const char* pair_env = getenv("MBX_PAIR");
+    const size_t kv_bytes = (size_t)g.bh * g.gk * g.s1 * g.s2 * (size_t)(g.d + g.dv) * 2;
+    const bool pair = pair_env ? pair_env[0] == '1'
+                               : g.gq == 1 || (g.gq % 2 == 1 && kv_bytes <= ((size_t)48 << 20));
+    const int smem_pair = RowPSmem::kTotal + 1024;
+    if (pair && (e = cudaFuncSetAttribute(tc_row_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair)) !=
+                    cudaSuccess)
+        return e;
+    const int64_t pair_tasks = (int64_t)g.bh * ((g.gq * g.s1 + 1) / 2) * g.gk;
+    const int grid_pair = pair_tasks < sms ? (int)pair_tasks : sms;
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
     const int grid_col = ngroups < sms ? (int)ngroups : sms;
     const int64_t aitems = ncols * ((g.nkeys + kAKC - 1) / kAKC);
@@ -435,7 +457,11 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1)
     for (int t = 0; t < g.T; ++t) {
         int last = t == g.T - 1, amode = t > 0, mode = last ? 0 : 1;
-        {
+        if (pair) {
+            ProfScope p("tc_row_pair", stream);
+            void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
+            if ((e = launch((const void*)tc_row_pair, grid_pair, 448, smem_pair, args)) != cudaSuccess) return e;
+        } else {
             ProfScope p("tc_row_stage", stream);
             void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
             if ((e = launch((const void*)tc_row_stage, grid_row, kRowThreads, smem_row, args)) != cudaSuccess) return e;

@@ -1,0 +1,417 @@
+// Row stage, half-packed variant (included by mbx_tc.cu).  A 128-lane M tile of the
+// classic row stage holds whole query tiles (s2 <= 64 rows each), so a plan with one
+// (or an odd number of) query tiles leaves up to 60% of every softmax / epilogue pass
+// idle.  Here a task is two independent M=64 "halves", each one (query tile qt, in-tile
+// row k) combination of the same (b,h) and key tile c, with its own K/V row (c,k): the
+// two MMAs' accumulators interleave in TMEM (M=64 row r -> lane 32 (r / 16) + r % 16,
+// the second MMA at lane offset 16), so every 128-lane pass carries 2 s2 useful rows.
+// Halves enumerate idx = k * G_q + qt; task pair p holds idx 2p, 2p+1, and halves with the
+// same k share one K/V ring stage.  Per task:
+//   MMA1  S_h = A_h . K_{c,k_h}^T     2 x (64 x 64 x 128)  A = Q (or hat_alpha_R) rows from smem
+//   softmax over i (warps 2-5), c_L to the workspace, P (bf16) back over S
+//   MMA2  [aL | Y]_h = P_h . [K | V]_{c,k_h}   2 x 2 x (64 x 128 x 64), A = P in TMEM
+//   epilogue: warps 6-9 (aL) / 10-13 (Y), per warp two 16-row TMA stores (one per half)
+// (solver.py:187-191 R update and c_L; factors.py:123 Y = R V)
+constexpr int kPKV = 4;   // K/V ring stages (one key row each)
+struct RowPSmem {
+    static constexpr int kA = 0;                         // A slots [2] x [2 d-chunks][2 halves][64 rows][128 B]
+    static constexpr int kASlot = 32768;
+    static constexpr int kKV = 2 * kASlot;               // K/V rows [4] x [K c0 | K c1 | V c0 | V c1]
+    static constexpr int kKVBytes = 32768;
+    static constexpr int kStage = kKV + kPKV * kKVBytes; // staging [8 warps] x [32 rows][64] bf16
+    static constexpr int kBars = kStage + 8 * 4096;
+    static constexpr int kNumBars = 4 + 2 * kPKV + 8;
+    static constexpr int kTmemSlot = kBars + kNumBars * 8;
+    static constexpr int kTotal = kTmemSlot + 16;
+};
+static_assert(RowPSmem::kTotal + 1024 <= 232448, "paired row stage exceeds 227 KB of shared memory");
+// TMEM: S/P buffers [0,64) [64,128); O_aL [128,256); O_Y [256,384)
+constexpr uint32_t kPS = 0, kPOA = 128, kPOY = 256;
+
+// Task walker: tasks (bh, p, c) in order, a contiguous range per CTA; item = (bh, p).
+// Half h of pair p is idx = 2p + h = k * G_q + qt (valid while idx < G_q * s1).
+struct PairCursor {
+    int t, t1, bh, kp, c, n_kp, gk, gq, nidx;
+    int k0, q0, k1, q1;       // (row, query tile) of the two halves
+    int kvi, kst, kph;        // K/V ring position of this task's first row
+    bool valid;
+    __device__ __forceinline__ void halves() {
+        k0 = (2 * kp) / gq;
+        q0 = 2 * kp - k0 * gq;
+        q1 = q0 + 1;
+        k1 = k0;
+        if (q1 == gq) {
+            q1 = 0;
+            ++k1;
+        }
+    }
+    __device__ __forceinline__ void init(const Geometry& g, int cta, int ctas) {
+        gq = g.gq;
+        nidx = g.gq * g.s1;
+        n_kp = (nidx + 1) / 2;
+        gk = g.gk;
+        const long long tasks = (long long)g.bh * n_kp * g.gk;
+        t = (int)(tasks * cta / ctas);
+        t1 = (int)(tasks * (cta + 1) / ctas);
+        c = t % gk;
+        kp = (t / gk) % n_kp;
+        bh = t / (gk * n_kp);
+        halves();
+        kvi = kst = kph = 0;
+        valid = t < t1;
+    }
+    __device__ __forceinline__ int nh() const { return 2 * kp + 1 < nidx ? 2 : 1; }   // valid halves
+    __device__ __forceinline__ int nrows() const { return nh() == 2 && k1 != k0 ? 2 : 1; }   // distinct K/V rows
+    __device__ __forceinline__ int kr(int hh) const { return hh ? k1 : k0; }
+    __device__ __forceinline__ int qt(int hh) const { return hh ? q1 : q0; }
+    __device__ __forceinline__ bool first_of_item(int t0) const { return c == 0 || t == t0; }
+    __device__ __forceinline__ bool last_of_item() const { return c == gk - 1 || t == t1 - 1; }
+    __device__ __forceinline__ void advance() {
+        for (int h = nrows(); h > 0; --h) {
+            ++kvi;
+            if (++kst == kPKV) {
+                kst = 0;
+                kph ^= 1;
+            }
+        }
+        ++t;
+        valid = t < t1;
+        if (++c == gk) {
+            c = 0;
+            if (++kp == n_kp) {
+                kp = 0;
+                ++bh;
+            }
+            halves();
+        }
+    }
+};
+
+__global__ void __launch_bounds__(448, 1)
+tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int want_y_i) {
+    const bool amode = amode_i != 0, want_y = want_y_i != 0;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RowPSmem::kBars);
+    uint64_t* a_full = bars;                       // [2] A slot landed (Q per item, hat_alpha_R per task)
+    uint64_t* a_empty = bars + 2;                  // [2] MMA1s done with it
+    uint64_t* kv_full = bars + 4;                  // [4]
+    uint64_t* kv_empty = kv_full + kPKV;           // [4]
+    uint64_t* s_full = kv_empty + kPKV;            // [2]
+    uint64_t* p_full = s_full + 2;                 // [2]
+    uint64_t* o_full = p_full + 2;                 // [2]
+    uint64_t* o_empty = o_full + 2;                // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowPSmem::kTmemSlot);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const uint32_t box_bytes = (uint32_t)g.s2 * 128u;
+    const int ckey = ckey_stride(g);
+    SPAN_AT(0, 0);
+
+    if (tid == 0) {
+        tma_prefetch(&P.tq);
+        tma_prefetch(&P.tk);
+        tma_prefetch(&P.tv);
+        tma_prefetch(&P.tws16);
+        tma_prefetch(&P.tws16r);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 128);
+        }
+        for (int i = 0; i < kPKV; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        fence_barrier_init();
+    }
+    // K/V rows s2..63 and A rows s2..63 are never written by TMA: MMA2 multiplies K/V
+    // padding by P = 0 (must be finite); A padding only feeds rows that are never stored.
+    for (int i = tid; i < kPKV * RowPSmem::kKVBytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem + RowPSmem::kKV)[i] = make_uint4(0, 0, 0, 0);
+    if (warp == 0) tmem_alloc<512>(tmem_slot);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();
+
+    PairCursor cur;
+    cur.init(g, blockIdx.x, gridDim.x);
+    const int t0 = cur.t;
+    int ti = 0;   // trace event index (MBX_TRACE builds)
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (whole warp, elected lane issues)
+        const bool leader = elect_one();
+        // A slot of (item or task) n: the halves' Q rows (per item) or hat_alpha_R rows (per task)
+        int an = 0;
+        auto load_a = [&](const PairCursor& pc) {
+            const int sl = an & 1;
+            mbar_wait(&a_empty[sl], ((an >> 1) & 1) ^ 1);
+            const int b = pc.bh / g.heads, h = pc.bh % g.heads, nh = pc.nh();
+            if (leader) {
+                mbar_expect_tx(&a_full[sl], 2u * box_bytes * (uint32_t)nh);
+                uint8_t* ab = smem + RowPSmem::kA + sl * RowPSmem::kASlot;
+                for (int hh = 0; hh < nh; ++hh) {
+                    const int kr = pc.kr(hh), qt = pc.qt(hh);
+                    if (amode) {
+                        const int key = pc.c * g.s1 + kr, ag = pc.bh * g.gq + qt;
+                        tma_load_4d(ab + hh * 8192, &P.tar_ld, &a_full[sl], 0, 0, key, ag);
+                        tma_load_4d(ab + 16384 + hh * 8192, &P.tar_ld, &a_full[sl], 64, 0, key, ag);
+                    } else {
+                        const int tok = (int)row_base(g, true, qt, kr);
+                        tma_load_4d(ab + hh * 8192, &P.tq, &a_full[sl], 0, tok, h, b);
+                        tma_load_4d(ab + 16384 + hh * 8192, &P.tq, &a_full[sl], 64, tok, h, b);
+                    }
+                }
+            }
+            __syncwarp();
+            ++an;
+        };
+        PairCursor pc = cur;
+        while (pc.valid) {
+            if (amode || pc.first_of_item(t0)) {
+                load_a(pc);
+                if (leader) TR(0, ti, 1);
+            }
+            const int b = pc.bh / g.heads, h = pc.bh % g.heads;
+            int kvi = pc.kvi, kst = pc.kst, kph = pc.kph;
+            for (int r = 0; r < pc.nrows(); ++r) {
+                mbar_wait(&kv_empty[kst], kph ^ 1);
+                const int tok = (int)row_base(g, false, pc.c, pc.kr(r));
+                if (leader) {
+                    mbar_expect_tx(&kv_full[kst], 4u * box_bytes);
+                    uint8_t* kb = smem + RowPSmem::kKV + kst * RowPSmem::kKVBytes;
+                    tma_load_4d(kb, &P.tk, &kv_full[kst], 0, tok, h, b);
+                    tma_load_4d(kb + 8192, &P.tk, &kv_full[kst], 64, tok, h, b);
+                    tma_load_4d(kb + 16384, &P.tv, &kv_full[kst], 0, tok, h, b);
+                    tma_load_4d(kb + 24576, &P.tv, &kv_full[kst], 64, tok, h, b);
+                }
+                if (leader) TR(0, ti, 2);
+                __syncwarp();
+                ++kvi;
+                if (++kst == kPKV) {
+                    kst = 0;
+                    kph ^= 1;
+                }
+            }
+            pc.advance();
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (whole warp, uniform descriptors)
+        const bool leader = elect_one();
+        const uint32_t id1 = idesc_bf16(64, 64, false, false);
+        const uint32_t id2 = idesc_bf16(64, 128, false, true);
+        constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+        auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
+        const uint32_t a_lo = ((smem_u32(smem + RowPSmem::kA) & 0x3FFFF) >> 4) | (1u << 16);
+        const uint32_t kv_lo = (smem_u32(smem + RowPSmem::kKV) & 0x3FFFF) >> 4;
+        PairCursor cs = cur, co = cur;
+        int ts = 0, to = 0, an_s = 0;   // an_s: A slot uses consumed by MMA1
+        while (cs.valid || co.valid) {
+            // MMA2(to): softmax done with S/P buffer to%2, O buffers drained by task to-1
+            if (co.valid && to < ts && mbar_test_uniform(&p_full[to & 1], (to >> 1) & 1) &&
+                mbar_test_uniform(&o_empty[0], (to & 1) ^ 1) &&
+                (!want_y || mbar_test_uniform(&o_empty[1], (to & 1) ^ 1))) {
+                if (leader) TR(1, ti, 13);
+                tc_fence_after();
+                if (leader) {
+                    const int two = co.nrows() == 2;
+                    for (int hh = 0; hh < co.nh(); ++hh) {
+                        int kst = co.kst + (hh & two);
+                        if (kst >= kPKV) kst -= kPKV;
+                        const uint32_t lane_h = (uint32_t)(hh * 16) << 16;
+                        const uint32_t b_lo = kv_lo + (uint32_t)kst * (RowPSmem::kKVBytes >> 4) + (8192u >> 4 << 16);
+                        const uint32_t pa = tmem + kPS + (to & 1) * 64 + lane_h;
+                        for (int s = 0; s < (want_y ? 2 : 1); ++s) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_bf16_ts(tmem + (s ? kPOY : kPOA) + lane_h, pa + kk * 8,
+                                            desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), id2, kk > 0);
+                        }
+                        if (hh == co.nh() - 1 || two) mma_commit(&kv_empty[kst]);
+                    }
+                    mma_commit(&o_full[0]);
+                    if (want_y) mma_commit(&o_full[1]);
+                    TR(1, ti, 12);
+                }
+                __syncwarp();
+                co.advance();
+                ++to;
+            }
+            // MMA1(ts): S/P buffer ts%2 released by MMA2(ts-2), A slot and K/V rows landed
+            if (cs.valid && ts < to + 2) {
+                const int sl = an_s & 1;
+                bool ready = mbar_test_uniform(&a_full[sl], (an_s >> 1) & 1);
+                int kst = cs.kst, kph = cs.kph;
+                for (int r = 0; r < cs.nrows() && ready; ++r) {
+                    ready = mbar_test_uniform(&kv_full[kst], kph);
+                    if (++kst == kPKV) {
+                        kst = 0;
+                        kph ^= 1;
+                    }
+                }
+                if (ready) {
+                    if (leader) TR(1, ti, 10);
+                    tc_fence_after();
+                    const bool last_use = amode || cs.last_of_item();
+                    if (leader) {
+                        const int two = cs.nrows() == 2;
+                        for (int hh = 0; hh < cs.nh(); ++hh) {
+                            int ks = cs.kst + (hh & two);
+                            if (ks >= kPKV) ks -= kPKV;
+                            const uint32_t aa = a_lo + (uint32_t)sl * (RowPSmem::kASlot >> 4) + ((hh * 8192) >> 4);
+                            const uint32_t b_lo = kv_lo + (uint32_t)ks * (RowPSmem::kKVBytes >> 4) + (1u << 16);
+                            const uint32_t d = tmem + kPS + (ts & 1) * 64 + ((uint32_t)(hh * 16) << 16);
+#pragma unroll
+                            for (int kk = 0; kk < 8; ++kk)
+                                mma_bf16(d, desc(aa + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
+                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), id1, kk > 0);
+                        }
+                        mma_commit(&s_full[ts & 1]);
+                        if (last_use) mma_commit(&a_empty[sl]);
+                        TR(1, ti, 11);
+                    }
+                    __syncwarp();
+                    if (last_use) ++an_s;
+                    cs.advance();
+                    ++ts;
+                }
+            }
+        }
+    } else if (warp < 6) {
+        // ------------------------------------------------ softmax: lane = (half h, row j)
+        const int quad = warp & 3;
+        const int hh = lane >> 4, j = quad * 16 + (lane & 15);
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const float sl2 = g.scale * kLog2e;
+        for (int t = 0; cur.valid; ++t, cur.advance()) {
+            const int bsel = t & 1;
+            const uint32_t sbuf = tmem + kPS + bsel * 64 + lane_off;
+            const int kr = cur.kr(hh), qt = cur.qt(hh);
+            const bool row_ok = j < g.s2 && hh < cur.nh();
+            mbar_wait(&s_full[bsel], (t >> 1) & 1);
+            if (lane == 0) TR(warp, ti, 21);
+            tc_fence_after();
+            float z[64];
+            {
+                uint32_t zr[64];
+                tmem_ld32_nw(sbuf, zr);
+                tmem_ld32_nw(sbuf + 32, zr + 32);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 64; ++i) z[i] = __uint_as_float(zr[i]);
+            }
+#pragma unroll
+            for (int blk = 0; blk < 4; ++blk) {   // only the 16-column blocks that reach past s2
+                if (16 * blk + 16 > g.s2) {
+#pragma unroll
+                    for (int i = 16 * blk; i < 16 * blk + 16; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+                }
+            }
+            float mq[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) mq[e] = fmaxf(z[e], z[e + 8]);
+#pragma unroll
+            for (int i = 16; i < 64; i += 8)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) mq[e] = fmaxf(mq[e], z[i + e]);
+            const float m = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                  fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+            const float mb = m * sl2;
+            float p[64];
+#pragma unroll
+            for (int i = 0; i < 64; ++i) p[i] = ex2(fmaf(z[i], sl2, -mb));
+            float lq[8], aq[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                lq[e] = p[e] + p[e + 8];
+                aq[e] = fmaf(p[e + 8], z[e + 8], p[e] * z[e]);
+            }
+#pragma unroll
+            for (int i = 16; i < 64; i += 8)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    lq[e] += p[i + e];
+                    aq[e] = fmaf(p[i + e], z[i + e], aq[e]);
+                }
+            const float l = ((lq[0] + lq[1]) + (lq[2] + lq[3])) + ((lq[4] + lq[5]) + (lq[6] + lq[7]));
+            const float A = ((aq[0] + aq[1]) + (aq[2] + aq[3])) + ((aq[4] + aq[5]) + (aq[6] + aq[7]));
+            const float inv_l = 1.f / l;
+            const float pscale = row_ok ? inv_l : 0.f;
+            uint32_t packed[32];
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(p[i] * pscale, p[i + 1] * pscale);
+            tmem_st32(sbuf, reinterpret_cast<const float*>(packed));
+            tc_fence_before();
+            mbar_arrive(&p_full[bsel]);
+            if (lane == 0) TR(warp, ti, 22);
+            if (row_ok) {   // c_L = sum R z - lse with z = scale * S (solver.py:191)
+                const int col = (cur.bh * g.gq + qt) * g.s2 + j;
+                P.wc[(int64_t)col * ckey + cur.c * g.s1 + kr] = g.scale * (A * inv_l - m) - __logf(l);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue: warps 6-9 O_aL, 10-13 O_Y
+        const int set = warp >= 10 ? 1 : 0;
+        if (set == 1 && !want_y) cur.valid = false;
+        const int quad = warp & 3;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
+        const int nr = min(16, g.s2 - quad * 16);             // rows j of this warp (per half)
+        const CUtensorMap* map = nr == 16 ? &P.tws16 : &P.tws16r;
+        uint8_t* stg = smem + RowPSmem::kStage + (warp - 6) * 4096;
+        for (int t = 0; cur.valid; ++t, cur.advance()) {
+            const int nh = cur.nh();
+            const bool store_ok = nr > 0;
+            const int col0 = (cur.bh * g.gq) * g.s2 + quad * 16;   // + qt_h * s2 per half
+            mbar_wait(&o_full[set], t & 1);
+            if (lane == 0) TR(warp, ti, 31);
+            tc_fence_after();
+            uint32_t pk[2][32];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t o[32];
+                tmem_ld32_nw(obuf + q4 * 32, o);
+                tmem_wait_ld();
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    pk[q4 >> 1][(q4 & 1) * 16 + i] = pack_bf16(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+            }
+            tc_fence_before();
+            mbar_arrive(&o_empty[set]);
+            if (lane == 0) TR(warp, ti, 32);
+            if (store_ok) {
+#pragma unroll
+                for (int part = 0; part < 2; ++part) {
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+                    const uint32_t srow = smem_u32(stg) + lane * 128;
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc)
+                        st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pk[part][4 * cc], pk[part][4 * cc + 1],
+                                     pk[part][4 * cc + 2], pk[part][4 * cc + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (int hh = 0; hh < nh; ++hh)   // rows 16 hh .. of the staging: half hh (key row k_hh)
+                            tma_store_4d(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
+                                         col0 + cur.qt(hh) * g.s2);
+                        bulk_commit();
+                    }
+                }
+            }
+        }
+        if (lane == 0) bulk_wait<0>();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+    SPAN_AT(0, 1);
+}

@@ -89,6 +89,23 @@ __global__ void probe(long long* out, int iters) {
                                smem_desc(sb + h * 16384 + kk * 2048, 8192, 1024, 2), id2, kk > 0);
                     mma_commit(&bar2[1 + h]);
                 }
+            } else if (MODE == 8) {   // M=64 pair task: 2 x MMA1 (64x64xK128 SS) + 4 x MMA2 (64x128xK64 TS)
+                const uint32_t i64a = idesc_bf16(64, 64, false, false), i64b = idesc_bf16(64, 128, false, true);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_bf16(tmem + (uint32_t)(hh * 16 << 16) + (it & 1) * 64,
+                                 smem_desc(sa + hh * 8192 + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, 2),
+                                 smem_desc(sb + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024, 2), i64a, kk > 0);
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int s = 0; s < 2; ++s)
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            mma_ts(tmem + (uint32_t)(hh * 16 << 16) + 128 + s * 128, tmem + (uint32_t)(hh * 16 << 16) + (it & 1) * 64 + kk * 8,
+                                   smem_desc(sb + s * 16384 + kk * 2048, 8192, 1024, 2), i64b, kk > 0);
             } else {   // big GEMM shape 128x256 K=64, both K-major
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
@@ -131,5 +148,6 @@ int main() {
     run<5>("row task with 4 commits", 128.0 * 64 * 128 + 2 * 128.0 * 128 * 64);
     run<6>("row MMA1 128x64xK128 TS (A tmem)", 128.0 * 64 * 128);
     run<7>("row task TS/TS exact with commits", 128.0 * 64 * 128 + 2 * 128.0 * 128 * 64);
+    run<8>("M=64 pair task (2x MMA1 64x64x128 SS, 4x MMA2 64x128x64 TS)", 128.0 * 64 * 128 + 2 * 128.0 * 128 * 64);
     return 0;
 }

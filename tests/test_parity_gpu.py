@@ -233,3 +233,33 @@ def test_wide_column_path(cuda, frames, q_frames, nb, H, T):
     out = ops.forward(q, k, v, low, T)
     ref = _oracle_heads(q, k, v, low, T)
     assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("row_stage", ["0", "1"])
+@pytest.mark.parametrize("frames,q_frames,h,nb,T", [(3, 3, 30, None, 1), (5, 3, 30, None, 2), (2, 2, 30, None, 1),
+                                                    (4, 4, 30, None, 1), (3, 3, 30, (3, 30, 52), 1),
+                                                    (3, 3, 30, "raw", 2), (7, 3, 30, None, 3), (3, 3, 15, None, 2)])
+def test_row_stage_variants(cuda, monkeypatch, row_stage, frames, q_frames, h, nb, T):
+    """Both row-stage kernels -- the classic one (whole query tiles per M=128 task)
+    and the half-packed one (two M=64 (query tile, row) halves per task, halves with
+    the same row sharing one K/V stage) -- on G_q = 1, 2, 3, 4, a raw (117, 40) blocking
+    (odd s1: a lone last half) and G_q s1 = 3 x 15 odd, against the oracle.  MBX_PAIR
+    forces the variant (read on every forward)."""
+    monkeypatch.setenv("MBX_PAIR", row_stage)
+    g = torch.Generator(device="cpu").manual_seed(frames * 13 + q_frames + 7 * T + h)
+    w = 52
+    shape = pk.VideoShape(frames, h, w)
+    if nb is None:
+        plan = _sf_plan(frames, h, w)
+    elif nb == "raw":
+        plan = pk.config_from_sizes(shape, 117, 40)
+    else:
+        plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
+    low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
+    q = torch.randn(1, 2, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k = torch.randn(1, 2, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    v = torch.randn(1, 2, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    assert ops.selected_path(q, k, v, low, T) == "tcgen05"
+    out = ops.forward(q, k, v, low, T)
+    ref = _oracle_heads(q, k, v, low, T)
+    assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
