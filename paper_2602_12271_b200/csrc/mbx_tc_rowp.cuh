@@ -13,6 +13,7 @@
 //   epilogue: warps 6-9 (aL) / 10-13 (Y), per warp two 16-row TMA stores (one per half)
 // (solver.py:187-191 R update and c_L; factors.py:123 Y = R V)
 constexpr int kPKV = 4;   // K/V ring stages (one key row each)
+constexpr int kPSB = 3;   // S/P buffers: MMA1 runs up to three tasks ahead of MMA2
 struct RowPSmem {
     static constexpr int kA = 0;                         // A slots [2] x [2 d-chunks][2 halves][64 rows][128 B]
     static constexpr int kASlot = 32768;
@@ -20,13 +21,13 @@ struct RowPSmem {
     static constexpr int kKVBytes = 32768;
     static constexpr int kStage = kKV + kPKV * kKVBytes; // staging [8 warps] x [32 rows][64] bf16
     static constexpr int kBars = kStage + 8 * 4096;
-    static constexpr int kNumBars = 4 + 2 * kPKV + 8;
+    static constexpr int kNumBars = 4 + 2 * kPKV + 2 * kPSB + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
 static_assert(RowPSmem::kTotal + 1024 <= 232448, "paired row stage exceeds 227 KB of shared memory");
-// TMEM: S/P buffers [0,64) [64,128); O_aL [128,256); O_Y [256,384)
-constexpr uint32_t kPS = 0, kPOA = 128, kPOY = 256;
+// TMEM: S/P buffers [0,64) [64,128) [128,192); O_aL [192,320); O_Y [320,448)
+constexpr uint32_t kPS = 0, kPOA = 64 * kPSB, kPOY = kPOA + 128;
 
 // Task walker: tasks (bh, p, c) in order, a contiguous range per CTA; item = (bh, p).
 // Half h of pair p is idx = 2p + h = k * G_q + qt (valid while idx < G_q * s1).
@@ -97,9 +98,9 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     uint64_t* a_empty = bars + 2;                  // [2] MMA1s done with it
     uint64_t* kv_full = bars + 4;                  // [4]
     uint64_t* kv_empty = kv_full + kPKV;           // [4]
-    uint64_t* s_full = kv_empty + kPKV;            // [2]
-    uint64_t* p_full = s_full + 2;                 // [2]
-    uint64_t* o_full = p_full + 2;                 // [2]
+    uint64_t* s_full = kv_empty + kPKV;            // [3]
+    uint64_t* p_full = s_full + kPSB;              // [3]
+    uint64_t* o_full = p_full + kPSB;              // [2]
     uint64_t* o_empty = o_full + 2;                // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowPSmem::kTmemSlot);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -114,13 +115,17 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         tma_prefetch(&P.tv);
         tma_prefetch(&P.tws16);
         tma_prefetch(&P.tws16r);
+        tma_prefetch(&P.tws);
+        tma_prefetch(&P.tws_b);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
-            mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 128);
             mbar_init(&o_full[i], 1);
             mbar_init(&o_empty[i], 128);
+        }
+        for (int i = 0; i < kPSB; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
         }
         for (int i = 0; i < kPKV; ++i) {
             mbar_init(&kv_full[i], 1);
@@ -208,34 +213,40 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         const bool leader = elect_one();
         const uint32_t id1 = idesc_bf16(64, 64, false, false);
         const uint32_t id2 = idesc_bf16(64, 128, false, true);
+        const uint32_t id1w = idesc_bf16(128, 64, false, false);    // shared-row tasks: one M=128 MMA
+        const uint32_t id2w = idesc_bf16(128, 128, false, true);
         constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
         auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
         const uint32_t a_lo = ((smem_u32(smem + RowPSmem::kA) & 0x3FFFF) >> 4) | (1u << 16);
         const uint32_t kv_lo = (smem_u32(smem + RowPSmem::kKV) & 0x3FFFF) >> 4;
         PairCursor cs = cur, co = cur;
         int ts = 0, to = 0, an_s = 0;   // an_s: A slot uses consumed by MMA1
+        int sb_s = 0, sph_s = 0, sb_o = 0, sph_o = 0;   // S/P buffer + phase of task ts / to
         while (cs.valid || co.valid) {
             // MMA2(to): softmax done with S/P buffer to%2, O buffers drained by task to-1
-            if (co.valid && to < ts && mbar_test_uniform(&p_full[to & 1], (to >> 1) & 1) &&
+            if (co.valid && to < ts && mbar_test_uniform(&p_full[sb_o], sph_o) &&
                 mbar_test_uniform(&o_empty[0], (to & 1) ^ 1) &&
                 (!want_y || mbar_test_uniform(&o_empty[1], (to & 1) ^ 1))) {
                 if (leader) TR(1, ti, 13);
                 tc_fence_after();
                 if (leader) {
                     const int two = co.nrows() == 2;
-                    for (int hh = 0; hh < co.nh(); ++hh) {
+                    const bool wide = co.nh() == 2 && !two;   // both halves on one K/V row: M=128
+                    const int nm = wide ? 1 : co.nh();
+                    const uint32_t id = wide ? id2w : id2;
+                    for (int hh = 0; hh < nm; ++hh) {
                         int kst = co.kst + (hh & two);
                         if (kst >= kPKV) kst -= kPKV;
                         const uint32_t lane_h = (uint32_t)(hh * 16) << 16;
                         const uint32_t b_lo = kv_lo + (uint32_t)kst * (RowPSmem::kKVBytes >> 4) + (8192u >> 4 << 16);
-                        const uint32_t pa = tmem + kPS + (to & 1) * 64 + lane_h;
+                        const uint32_t pa = tmem + kPS + sb_o * 64 + lane_h;
                         for (int s = 0; s < (want_y ? 2 : 1); ++s) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
                                 mma_bf16_ts(tmem + (s ? kPOY : kPOA) + lane_h, pa + kk * 8,
-                                            desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), id2, kk > 0);
+                                            desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), id, kk > 0);
                         }
-                        if (hh == co.nh() - 1 || two) mma_commit(&kv_empty[kst]);
+                        if (hh == nm - 1 || two) mma_commit(&kv_empty[kst]);
                     }
                     mma_commit(&o_full[0]);
                     if (want_y) mma_commit(&o_full[1]);
@@ -244,9 +255,13 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 __syncwarp();
                 co.advance();
                 ++to;
+                if (++sb_o == kPSB) {
+                    sb_o = 0;
+                    sph_o ^= 1;
+                }
             }
             // MMA1(ts): S/P buffer ts%2 released by MMA2(ts-2), A slot and K/V rows landed
-            if (cs.valid && ts < to + 2) {
+            if (cs.valid && ts < to + kPSB) {
                 const int sl = an_s & 1;
                 bool ready = mbar_test_uniform(&a_full[sl], (an_s >> 1) & 1);
                 int kst = cs.kst, kph = cs.kph;
@@ -263,18 +278,21 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     const bool last_use = amode || cs.last_of_item();
                     if (leader) {
                         const int two = cs.nrows() == 2;
-                        for (int hh = 0; hh < cs.nh(); ++hh) {
+                        const bool wide = cs.nh() == 2 && !two;   // rows of both halves stacked: M=128
+                        const int nm = wide ? 1 : cs.nh();
+                        const uint32_t id = wide ? id1w : id1;
+                        for (int hh = 0; hh < nm; ++hh) {
                             int ks = cs.kst + (hh & two);
                             if (ks >= kPKV) ks -= kPKV;
                             const uint32_t aa = a_lo + (uint32_t)sl * (RowPSmem::kASlot >> 4) + ((hh * 8192) >> 4);
                             const uint32_t b_lo = kv_lo + (uint32_t)ks * (RowPSmem::kKVBytes >> 4) + (1u << 16);
-                            const uint32_t d = tmem + kPS + (ts & 1) * 64 + ((uint32_t)(hh * 16) << 16);
+                            const uint32_t d = tmem + kPS + sb_s * 64 + ((uint32_t)(hh * 16) << 16);
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk)
                                 mma_bf16(d, desc(aa + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
-                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), id1, kk > 0);
+                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), id, kk > 0);
                         }
-                        mma_commit(&s_full[ts & 1]);
+                        mma_commit(&s_full[sb_s]);
                         if (last_use) mma_commit(&a_empty[sl]);
                         TR(1, ti, 11);
                     }
@@ -282,21 +300,28 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     if (last_use) ++an_s;
                     cs.advance();
                     ++ts;
+                    if (++sb_s == kPSB) {
+                        sb_s = 0;
+                        sph_s ^= 1;
+                    }
                 }
             }
         }
     } else if (warp < 6) {
         // ------------------------------------------------ softmax: lane = (half h, row j)
         const int quad = warp & 3;
-        const int hh = lane >> 4, j = quad * 16 + (lane & 15);
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const float sl2 = g.scale * kLog2e;
+        int bsel = 0, bph = 0;   // S/P buffer + phase of task t
         for (int t = 0; cur.valid; ++t, cur.advance()) {
-            const int bsel = t & 1;
             const uint32_t sbuf = tmem + kPS + bsel * 64 + lane_off;
+            // M=64 pair: lane = (half lane/16, row 16 quad + lane%16); shared-row M=128: (quad/2, 32 (quad%2) + lane)
+            const bool wide = cur.nh() == 2 && cur.nrows() == 1;
+            const int hh = wide ? quad >> 1 : lane >> 4;
+            const int j = wide ? 32 * (quad & 1) + lane : quad * 16 + (lane & 15);
             const int kr = cur.kr(hh), qt = cur.qt(hh);
             const bool row_ok = j < g.s2 && hh < cur.nh();
-            mbar_wait(&s_full[bsel], (t >> 1) & 1);
+            mbar_wait(&s_full[bsel], bph);
             if (lane == 0) TR(warp, ti, 21);
             tc_fence_after();
             float z[64];
@@ -356,6 +381,10 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 const int col = (cur.bh * g.gq + qt) * g.s2 + j;
                 P.wc[(int64_t)col * ckey + cur.c * g.s1 + kr] = g.scale * (A * inv_l - m) - __logf(l);
             }
+            if (++bsel == kPSB) {
+                bsel = 0;
+                bph ^= 1;
+            }
         }
     } else {
         // ------------------------------------------------ epilogue: warps 6-9 O_aL, 10-13 O_Y
@@ -364,12 +393,15 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
-        const int nr = min(16, g.s2 - quad * 16);             // rows j of this warp (per half)
+        const int nr = min(16, g.s2 - quad * 16);             // M=64 pair: rows j of this warp per half
         const CUtensorMap* map = nr == 16 ? &P.tws16 : &P.tws16r;
+        const int nrw = min(32, g.s2 - 32 * (quad & 1));      // shared-row M=128: rows of half quad/2
+        const CUtensorMap* mapw = (quad & 1) ? &P.tws_b : &P.tws;
         uint8_t* stg = smem + RowPSmem::kStage + (warp - 6) * 4096;
         for (int t = 0; cur.valid; ++t, cur.advance()) {
             const int nh = cur.nh();
-            const bool store_ok = nr > 0;
+            const bool wide = nh == 2 && cur.nrows() == 1;
+            const bool store_ok = wide ? nrw > 0 : nr > 0;
             const int col0 = (cur.bh * g.gq) * g.s2 + quad * 16;   // + qt_h * s2 per half
             mbar_wait(&o_full[set], t & 1);
             if (lane == 0) TR(warp, ti, 31);
@@ -400,9 +432,15 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        for (int hh = 0; hh < nh; ++hh)   // rows 16 hh .. of the staging: half hh (key row k_hh)
-                            tma_store_4d(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
-                                         col0 + cur.qt(hh) * g.s2);
+                        if (wide) {   // staging rows = j 32 (quad % 2) .. of half quad / 2
+                            const int hw = quad >> 1;
+                            tma_store_4d(mapw, stg, 0, cur.c * g.s1 + cur.kr(hw), 2 * set + part,
+                                         (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1));
+                        } else {
+                            for (int hh = 0; hh < nh; ++hh)   // rows 16 hh .. of the staging: half hh (key row k_hh)
+                                tma_store_4d(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
+                                             col0 + cur.qt(hh) * g.s2);
+                        }
                         bulk_commit();
                     }
                 }
