@@ -241,19 +241,33 @@ int row_ctas_override() {
 
 }  // namespace
 
-bool tc_supported(const Geometry& g, int dtype, int flags) {
-    if (flags & MBX_FLAG_FORCE_GENERIC) return false;
-    if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return false;
-    if (g.s2 > kMaxS2) return false;
-    if (g.T > 1 && g.s1 > 128) return false;   // alpha_R hand-off: query rows l on the MMA N axis
-    if (g.nf == 0 && (g.q_order || g.kv_order)) return false;   // rows need a closed form
+// Why a problem is not on the tcgen05 path (nullptr: it is); MBX_VERBOSE=1 prints it.
+static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags) {
+    if (flags & MBX_FLAG_FORCE_GENERIC) return "forced generic";
+    if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return "needs bf16 with d = dv = 128";
+    if (g.s2 > kMaxS2) return "s2 > 64";
+    if (g.T > 1 && g.s1 > 128) return "T > 1 with s1 > 128";   // alpha_R hand-off: query rows l on the MMA N axis
+    if (g.nf == 0 && (g.q_order || g.kv_order)) return "permuted plan without a closed form";
     int F, H, W;
-    if (!column_grid(g, &F, &H, &W)) return false;
-    if (!strides_ok(g.qs) || !strides_ok(g.ks) || !strides_ok(g.vs) || !strides_ok(g.os)) return false;
-    if (g.bh > 1 && g.qs[0] != (int64_t)g.heads * g.qs[1]) return false;   // qcol map folds (b, h)
-    if (g.bh > 1 && g.os[0] != (int64_t)g.heads * g.os[1]) return false;   // output map folds (b, h)
-    if ((int64_t)g.bh * g.gq * g.s2 * g.nkeys >= ((int64_t)1 << 31)) return false;
-    return encode_fn() != nullptr;
+    if (!column_grid(g, &F, &H, &W)) return "tile rows are not contiguous grid rows";
+    if (!strides_ok(g.qs) || !strides_ok(g.ks) || !strides_ok(g.vs) || !strides_ok(g.os))
+        return "strides not 16-byte aligned";
+    // the q-column / output maps fold (b, h) into one dim; a size-1 batch has no stride to fold
+    // (PyTorch keeps the parent's batch stride on head slices of a B = 1 tensor)
+    if (g.bh > g.heads && g.qs[0] != (int64_t)g.heads * g.qs[1]) return "q batch stride != heads * head stride";
+    if (g.bh > g.heads && g.os[0] != (int64_t)g.heads * g.os[1]) return "out batch stride != heads * head stride";
+    if ((int64_t)g.bh * g.gq * g.s2 * g.nkeys >= ((int64_t)1 << 31)) return "workspace rows exceed 2^31";
+    if (encode_fn() == nullptr) return "cuTensorMapEncodeTiled unavailable";
+    return nullptr;
+}
+
+bool tc_supported(const Geometry& g, int dtype, int flags) {
+    const char* why = tc_unsupported_reason(g, dtype, flags);
+    if (why && !(flags & MBX_FLAG_FORCE_GENERIC) && getenv("MBX_VERBOSE"))
+        fprintf(stderr, "mbx: tcgen05 path not used: %s (bh=%d heads=%d qs=%lld,%lld,%lld os=%lld,%lld,%lld)\n", why,
+                g.bh, g.heads, (long long)g.qs[0], (long long)g.qs[1], (long long)g.qs[2], (long long)g.os[0],
+                (long long)g.os[1], (long long)g.os[2]);
+    return why == nullptr;
 }
 
 size_t tc_workspace_bytes(const Geometry& g) {

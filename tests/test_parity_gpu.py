@@ -263,3 +263,18 @@ def test_row_stage_variants(cuda, monkeypatch, row_stage, frames, q_frames, h, n
     out = ops.forward(q, k, v, low, T)
     ref = _oracle_heads(q, k, v, low, T)
     assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
+
+
+def test_head_slices_of_single_batch_stay_on_tensor_cores(cuda):
+    """Head slices of a B = 1 tensor keep the parent's batch stride (PyTorch calls them
+    contiguous); a size-1 batch has nothing to fold, so they must still run on the
+    tcgen05 path -- and give the same rows as the full-head call."""
+    g = torch.Generator(device="cpu").manual_seed(11)
+    q, k, v = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    low = pk.lower_square(_sf_plan())
+    full = ops.forward(q, k, v, low, 1)
+    qs, ks, vs = (x[:, 1:3].contiguous() for x in (q, k, v))
+    assert qs.stride(0) == q.stride(0)
+    assert ops.selected_path(qs, ks, vs, low, 1) == "tcgen05"
+    part = ops.forward(qs, ks, vs, low, 1)
+    assert torch.equal(part, full[:, 1:3])
