@@ -86,6 +86,7 @@ struct TcParams {
     __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
+    int l2hint;                           // W stores evict_last, last reads evict_first (MBX_L2HINT=0: off)
 };
 
 // Row-stage query groups (<= 3 query tiles each) and key tiles per item; an
@@ -302,6 +303,8 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     {
         const char* e = getenv("MBX_DBG");
         P.dbg = e ? atoi(e) : 0;
+        const char* h = getenv("MBX_L2HINT");
+        P.l2hint = h ? atoi(h) : 1;
     }
     if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, g.s2) ||
         !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&P.tqc, q, g, nq) ||

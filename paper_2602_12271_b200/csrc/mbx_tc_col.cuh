@@ -121,6 +121,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         // whole warp on warp-uniform state (TMA coordinates in uniform registers), one elected lane issues
         const bool leader = elect_one();
         int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
+        // the final pass is W's last reader: stream it through L2 without displacing the rest
+        const uint64_t w_policy = P.l2hint && mode == 0 ? l2_evict_first() : l2_evict_normal();
         int ti = 0;
         auto next_slot = [&]() {
             if (++slot == kRing) {
@@ -144,8 +146,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     TRC(0, ti, 2);
                     mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                     uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
-                    tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0p + i);
-                    tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 3, col0p + i);
+                    tma_load_4d_hint(dst, &tm_w, &ring_full[slot], 0, k0, 2, col0p + i, w_policy);
+                    tma_load_4d_hint(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 3, col0p + i, w_policy);
                 }
                 __syncwarp();
                 next_slot();
@@ -190,8 +192,8 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     TRC(0, ti, 1);
                     mbar_expect_tx(&ring_full[slot], 2u * kKC * 128u);
                     uint8_t* dst = smem + ColSmem::kRingOff + slot * ColSmem::kSlot;
-                    tma_load_4d(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i);
-                    tma_load_4d(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i);
+                    tma_load_4d_hint(dst, &tm_w, &ring_full[slot], 0, k0, 0, col0 + i, w_policy);
+                    tma_load_4d_hint(dst + kKC * 128, &tm_w, &ring_full[slot], 0, k0, 1, col0 + i, w_policy);
                     mbar_expect_tx(&c_full[cb], kKC * 4u);
                     tma_load_2d(smem + ColSmem::kC + cb * 512, &tm_c, &c_full[cb], k0, col0 + i);
                 }

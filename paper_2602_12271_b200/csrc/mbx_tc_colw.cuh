@@ -92,6 +92,8 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
     if (warp == 0) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
+        // the final pass is W's last reader: stream it through L2 without displacing the rest
+        const uint64_t w_policy = P.l2hint && mode == 0 ? l2_evict_first() : l2_evict_normal();
         uint32_t n = 0;   // ring uses
         int u = 0;        // chunks
         for (int it = 0; it < my_items; ++it) {
@@ -117,8 +119,8 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
                     if (leader) {
                         mbar_expect_tx(&r_full[sl], 2u * kWKC * 128u);
                         uint8_t* dst = smem + WideSmem::kRing + sl * 32768;
-                        tma_load_4d(dst, &P.tw128, &r_full[sl], 0, k0, 2 * part, col);
-                        tma_load_4d(dst + 16384, &P.tw128, &r_full[sl], 0, k0, 2 * part + 1, col);
+                        tma_load_4d_hint(dst, &P.tw128, &r_full[sl], 0, k0, 2 * part, col, w_policy);
+                        tma_load_4d_hint(dst + 16384, &P.tw128, &r_full[sl], 0, k0, 2 * part + 1, col, w_policy);
                     }
                     __syncwarp();
                 }

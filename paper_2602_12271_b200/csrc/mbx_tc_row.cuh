@@ -137,6 +137,14 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
                  "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                  : "memory");
 }
+__device__ __forceinline__ void tma_store_4d_hint(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                  int c3, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(policy)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
@@ -524,6 +532,8 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
     } else {
         // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
         const int set = warp >= 10 ? 1 : 0;   // warps 6-9: O_aL, 10-13: O_Y
+        // the column stage reads W right after this launch: keep it in L2 ahead of q / k / v
+        const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
         if (set == 1 && !want_y) cur.valid = false;   // no Y this refinement
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
@@ -593,7 +603,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_4d(half ? &tm_wst_b : &tm_wst, stg, 0, key, 2 * set + part, col0);
+                        tma_store_4d_hint(half ? &tm_wst_b : &tm_wst, stg, 0, key, 2 * set + part, col0, w_policy);
                         bulk_commit();
                     }
                 }

@@ -390,6 +390,8 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         // ------------------------------------------------ epilogue: warps 6-9 O_aL, 10-13 O_Y
         const int set = warp >= 10 ? 1 : 0;
         if (set == 1 && !want_y) cur.valid = false;
+        // the column stage reads W right after this launch: keep it in L2 ahead of q / k / v
+        const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
@@ -434,12 +436,12 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     if (lane == 0) {
                         if (wide) {   // staging rows = j 32 (quad % 2) .. of half quad / 2
                             const int hw = quad >> 1;
-                            tma_store_4d(mapw, stg, 0, cur.c * g.s1 + cur.kr(hw), 2 * set + part,
-                                         (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1));
+                            tma_store_4d_hint(mapw, stg, 0, cur.c * g.s1 + cur.kr(hw), 2 * set + part,
+                                              (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1), w_policy);
                         } else {
                             for (int hh = 0; hh < nh; ++hh)   // rows 16 hh .. of the staging: half hh (key row k_hh)
-                                tma_store_4d(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
-                                             col0 + cur.qt(hh) * g.s2);
+                                tma_store_4d_hint(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
+                                                  col0 + cur.qt(hh) * g.s2, w_policy);
                         }
                         bulk_commit();
                     }
