@@ -89,19 +89,8 @@ struct TcParams {
     int l2hint;                           // W stores evict_last, last reads evict_first (MBX_L2HINT=0: off)
 };
 
-// Row-stage query groups (<= 3 query tiles each) and key tiles per item; an
-// exchange unit is (bh, query group, key-tile chunk) and is complete after
-// unit_signals(g) releases (12 per item: 4 softmax + 8 epilogue warps, s1 items).
+// Row-stage query groups (<= 3 query tiles each) of the classic row stage.
 __host__ __device__ __forceinline__ int row_groups(const Geometry& g) { return (g.gq + 2) / 3; }
-__host__ __device__ __forceinline__ int row_chunk(const Geometry& g) {
-    const int n = (g.gk + 6) / 7;
-    return (g.gk + n - 1) / n;
-}
-__host__ __device__ __forceinline__ unsigned unit_signals(const Geometry& g) { return 12u * (unsigned)g.s1; }
-__host__ __device__ __forceinline__ int exchange_units(const Geometry& g) {
-    const int cpi = row_chunk(g);
-    return g.bh * row_groups(g) * ((g.gk + cpi - 1) / cpi);
-}
 
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
@@ -117,32 +106,15 @@ __device__ __forceinline__ uint8_t* aligned_smem() {
 __global__ void __launch_bounds__(kRowThreads, 1)
 tc_row_stage(const __grid_constant__ TcParams P, Geometry g, int amode, int want_y) {
     SPAN_AT(0, 0);
-    row_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr, amode != 0, want_y != 0);
+    row_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, amode != 0, want_y != 0);
     SPAN_AT(0, 1);
 }
 
 __global__ void __launch_bounds__(kColThreads, 1)
 tc_column_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
     SPAN_AT(1, 0);
-    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, nullptr, mode);
+    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, mode);
     SPAN_AT(1, 1);
-}
-
-// One launch, both stages: CTAs [0, n_row) run the row stage, the rest the column
-// stage, which consumes each exchange unit as soon as its counter completes --
-// while the unit is still L2-resident -- and then discards its lines.  Needs all
-// CTAs co-resident (cooperative launch, one CTA per SM).
-__global__ void __launch_bounds__(kRowThreads, 1)
-tc_fused(const __grid_constant__ TcParams P, Geometry g, int n_row, unsigned* counters) {
-    if ((int)blockIdx.x < n_row) {
-        SPAN_AT(0, 0);
-        row_role(aligned_smem(), P, g, blockIdx.x, n_row, counters);
-        SPAN_AT(0, 1);
-    } else {
-        SPAN_AT(1, 0);
-        col_role(aligned_smem(), P, g, blockIdx.x - n_row, gridDim.x - n_row, counters);
-        SPAN_AT(1, 1);
-    }
 }
 
 // ===================================================================== host
@@ -226,18 +198,9 @@ bool column_grid(const Geometry& g, int* F, int* H, int* W) {
     return true;
 }
 
-// MBX_FUSED=1 selects the single-launch path; MBX_ROW_CTAS sets its row-stage CTA count.
-bool fused_enabled() {
-    const char* e = getenv("MBX_FUSED");
-    return e && e[0] == '1';
-}
 bool pdl_enabled() {   // MBX_PDL=0 disables programmatic dependent launch
     const char* e = getenv("MBX_PDL");
     return !(e && e[0] == '0');
-}
-int row_ctas_override() {
-    const char* e = getenv("MBX_ROW_CTAS");
-    return e ? atoi(e) : 0;
 }
 
 }  // namespace
@@ -273,8 +236,7 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
 
 size_t tc_workspace_bytes(const Geometry& g) {
     const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
-    size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4) +
-                   align256((size_t)exchange_units(g) * 4);
+    size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4);
     if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 2 * ((g.s1 + 31) / 32) * 32 * 4);
     return bytes;
 }
@@ -314,8 +276,6 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     const int64_t rows = ncols * g.nkeys;
     __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(workspace);
     float* Wc = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256(rows * 512));
-    unsigned* counters = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(Wc) +
-                                                     align256((size_t)ncols * ckey_stride(g) * 4));
     P.wc = Wc;
     P.w = Wp;
     P.stats = nullptr;
@@ -338,7 +298,7 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     }
     __nv_bfloat16* AR = nullptr;
     if (g.T > 1) {
-        char* after = reinterpret_cast<char*>(counters) + align256((size_t)exchange_units(g) * 4);
+        char* after = reinterpret_cast<char*>(Wc) + align256((size_t)ncols * ckey_stride(g) * 4);
         AR = reinterpret_cast<__nv_bfloat16*>(after);
         P.stats = reinterpret_cast<float*>(after + align256((size_t)rows * 256));
     }
@@ -394,29 +354,13 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
     cudaError_t e;
     const int smem_row = RowSmem::kTotal + 1024;
     const int smem_col = ColSmem::kTotal + 1024;
-    const int smem_fused = smem_row > smem_col ? smem_row : smem_col;
     if ((e = cudaFuncSetAttribute(tc_row_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_row)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(tc_column_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_col)) !=
         cudaSuccess)
         return e;
-    if ((e = cudaFuncSetAttribute(tc_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fused)) != cudaSuccess)
-        return e;
 
     const int sms = num_sms();
-    if (g.T == 1 && !wide && fused_enabled()) {
-        // split of the SMs between the stages (MBX_ROW_CTAS overrides)
-        int n_row = row_ctas_override();
-        if (n_row <= 0) n_row = (int)(sms * 0.55);
-        if (n_row < 1) n_row = 1;
-        if (n_row > sms - 1) n_row = sms - 1;
-        if ((e = cudaMemsetAsync(counters, 0, (size_t)exchange_units(g) * 4, stream)) != cudaSuccess) return e;
-        void* args[] = {(void*)&P, (void*)&g, (void*)&n_row, (void*)&counters};
-        ProfScope p("tc_fused", stream);
-        e = cudaLaunchCooperativeKernel((const void*)tc_fused, dim3(sms), dim3(kRowThreads), args, smem_fused, stream);
-        if (e == cudaSuccess) return cudaGetLastError();
-        cudaGetLastError();   // not co-resident here: fall back to two launches
-    }
     const int smem_alpha = AlphaSmem::kTotal + 1024;
     const int smem_wide = WideSmem::kTotal + 1024;
     if (wide && (e = cudaFuncSetAttribute(tc_column_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_wide)) !=

@@ -29,24 +29,11 @@ struct ColSmem {
     static constexpr int kTotal = kTmemSlot + 16;
 };
 
-// Waits until exchange unit u has all its row-stage signals, then orders the
-// subsequent TMA (async-proxy) reads after them.
-__device__ __forceinline__ void unit_wait(const unsigned* counters, int u, unsigned target) {
-    unsigned v;
-    while (true) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counters + u) : "memory");
-        if (v >= target) break;
-        __nanosleep(64);
-    }
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-// Column-stage role of CTA `first` among `stride` column CTAs.  counters != nullptr:
-// wait for each exchange unit before reading it and discard its L2 lines after use.
+// Column-stage role of CTA `first` among `stride` column CTAs.
 // mode 0: O = L Y (last refinement); mode 1 (T >= 2, earlier refinements): only the
 // per-row softmax statistics (running max, sum) of L, for the alpha_R stage.
 __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
-                                         const unsigned* counters, int mode = 0) {
+                                         int mode = 0) {
     const bool outm = mode == 0;
     const CUtensorMap& tm_w = P.tw;
     const CUtensorMap& tm_c = P.tc;
@@ -135,7 +122,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         const int U = my_groups * nch;
         // one-chunk lookahead only pays with several chunks per group (MBX_DBG 2048 / 4096 force off / on)
         const bool look = (nch > 1 || (P.dbg & 4096)) && !(P.dbg & 2048);
-        int bh = 0, a = 0, j0 = 0, col0 = 0, cc_done = -1;
+        int bh = 0, a = 0, j0 = 0, col0 = 0;
         auto load_y = [&](int up) {   // Y_i of chunk up (its group's columns col0p .. +3)
             int bhp, ap, j0p;
             decode(first + (up / nch) * stride, bhp, ap, j0p);
@@ -158,7 +145,6 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
             if (ch == 0) {
                 decode(first + gi * stride, bh, a, j0);
                 col0 = (bh * g.gq + a) * g.s2 + j0;
-                cc_done = -1;
                 mbar_wait(q_empty, (gi & 1) ^ 1);
                 if (leader) TRC(0, ti, 5);
                 const int64_t tq0 = row_base(g, true, a, 0) + j0;
@@ -175,15 +161,6 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 __syncwarp();
             }
             const int k0 = ch * kKC;
-            if (counters) {   // exchange units (bh, qg, cc) holding keys k0 .. k0 + kKC - 1
-                const int cpi = row_chunk(g), n_cc = (g.gk + cpi - 1) / cpi;
-                const int cc_hi = min(g.nkeys - 1, k0 + kKC - 1) / g.s1 / cpi;
-                const int ubase = (bh * row_groups(g) + a / kQG) * n_cc;
-                if (leader)
-                    for (int cc = cc_done + 1; cc <= cc_hi; ++cc) unit_wait(counters, ubase + cc, unit_signals(g));
-                __syncwarp();
-                cc_done = cc_hi;
-            }
             for (int i = 0; i < 4; ++i) {   // aL_i + c_L_i
                 mbar_wait(&ring_empty[slot], sph ^ 1);
                 const int cb = i * 2 + (u & 1);
@@ -449,15 +426,6 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     }
                 }
                 if (lane == 0) TRC(warp + 8, ti, 29);
-            }
-            if (counters) {   // this group's workspace lines are dead: drop them from L2 unwritten
-                for (int i = 0; i < 4; ++i) {
-                    if (j0 + i >= g.s2) break;
-                    const char* base = reinterpret_cast<const char*>(P.w) +
-                                       (size_t)((bh * g.gq + a) * g.s2 + j0 + i) * g.nkeys * 512 + quad * g.nkeys * 128;
-                    for (int ln = lane; ln < g.nkeys; ln += 32)
-                        asm volatile("discard.global.L2 [%0], 128;" ::"l"(base + (size_t)ln * 128) : "memory");
-                }
             }
             tc_fence_before();
             if (lane == 0) TRC(warp + 8, ti, 27);

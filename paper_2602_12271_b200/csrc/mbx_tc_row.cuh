@@ -40,12 +40,9 @@ static_assert(RowSmem::kTotal + 1024 <= 232448, "row stage exceeds 227 KB of sha
 // TMEM columns: Q M tiles [0,64) [64,128); S/P buffers [128,192) [192,256); O_aL [256,384); O_Y [384,512).
 constexpr uint32_t kRowQ = 0, kRowS = 128, kRowO = 256;
 
-// Walks the (item, key tile c, M tile mt) task sequence of one CTA.  Items are
-// ordered (b*h, query group qg, key-tile chunk cc, row k).  Two schedules:
-//  * round-robin items (single-launch path): the CTAs advance through the exchange
-//    units u = (bh, qg, cc) together, so each unit is consumed while L2-resident;
-//  * a contiguous range [L0, L1) of key rows (two-launch path; one chunk per item):
-//    equal key-row counts per CTA, the item's Q reloaded only at item boundaries.
+// Walks the (item, key tile c, M tile mt) task sequence of one CTA: a contiguous
+// range [L0, L1) of key rows, items ordered (b*h, query group qg, row k), equal
+// key-row counts per CTA, the item's Q reloaded only at item boundaries.
 struct RowCursor {
     int li, c, mt, kvi, n_mt, nt, bh, kr, qg, cc, c0, c1, unit, my_items, first, stride, n_qg, n_cc, cpi;
     int L0, L1;   // range schedule (stride == 0)
@@ -69,17 +66,6 @@ struct RowCursor {
             if (li == my_items - 1) c1 = (L1 - 1) % cpi + 1;
         }
         c = c0;
-    }
-    __device__ __forceinline__ void init(const Geometry& g, int first_, int stride_) {
-        first = first_;
-        stride = stride_;
-        n_qg = row_groups(g);
-        cpi = row_chunk(g);
-        n_cc = (g.gk + cpi - 1) / cpi;
-        const int items = g.bh * n_qg * n_cc * g.s1;
-        my_items = first < items ? (items - first + stride - 1) / stride : 0;
-        li = mt = kvi = kst = kph = 0;
-        load(g);
     }
     // Range schedule: CTA `cta` of `ctas` takes an equal share of all key rows.
     __device__ __forceinline__ void init_range(const Geometry& g, int cta, int ctas) {
@@ -161,21 +147,15 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"((uint32_t)accumulate));
 }
 
-// Release one signal on exchange unit u (after this thread's / warp's writes of it).
-__device__ __forceinline__ void unit_signal(unsigned* counters, int u) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counters + u) : "memory");
-}
-
 __device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
     asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc));
 }
 
-// Row-stage role of CTA `first` among `stride` row CTAs.  counters == nullptr: no
-// exchange signalling (two-launch path, contiguous key-row ranges).
+// Row-stage role of CTA `first` among `stride` row CTAs (contiguous key-row ranges).
 // amode: MMA1's A rows come from hat_alpha_R of the previous refinement (per task,
 // smem) instead of Q (per item, TMEM); want_y: compute Y = R V (last refinement only).
 __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
-                                         unsigned* counters, bool amode = false, bool want_y = true) {
+                                         bool amode = false, bool want_y = true) {
     const CUtensorMap& tm_q = P.tq;
     const CUtensorMap& tm_k = P.tk;
     const CUtensorMap& tm_v = P.tv;
@@ -246,10 +226,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
 
 #define WAITX(bar, par) do { if (P.dbg & 64) mbar_spin(bar, par); else if (P.dbg & 128) mbar_wait_nohint(bar, par); else mbar_wait(bar, par); } while (0)
     RowCursor cur;
-    if (counters)
-        cur.init(g, first, stride);
-    else
-        cur.init_range(g, first, stride);
+    cur.init_range(g, first, stride);
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -522,11 +499,6 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                 const int col = (cur.bh * g.gq + kQG * cur.qg + al) * g.s2 + j;
                 Wc[(int64_t)col * ckey + cur.c * g.s1 + cur.kr] = g.scale * (A * inv_l - m) - __logf(l);
             }
-            if (counters && cur.last_of_item()) {   // this warp's c_L of the item are written
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) unit_signal(counters, cur.unit);
-            }
             if (lane == 0) TR(warp, ti, 22);
         }
     } else {
@@ -543,24 +515,6 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
         uint8_t* stg_base = smem + RowSmem::kStage + (warp - 6) * 8192;
         int nstore = 0;   // staging buffer uses (== bulk groups committed) of this warp
         int ti = 0;
-        // An item is signalled once its TMA stores have completed; to keep stores in
-        // flight the wait is deferred until two newer groups exist (or forced).
-        int pend_u = -1, pend_g = 0;
-        auto flush = [&](bool force) {
-            if (pend_u < 0) return;
-            if (nstore - pend_g >= 2) {
-                if (lane == 0) bulk_wait<2>();
-            } else if (force) {
-                if (lane == 0) bulk_wait<0>();
-            } else {
-                return;
-            }
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                unit_signal(counters, pend_u);
-            }
-            pend_u = -1;
-        };
         for (int t = 0; cur.valid; ++t, cur.advance(g)) {
             const int al = cur.mt * 2 + (quad >> 1);
             const bool store_ok = al < cur.nt && nrows > 0;
@@ -608,18 +562,9 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     }
                 }
             }
-            if (counters) {
-                flush(false);
-                if (cur.last_of_item()) {
-                    flush(true);   // at most one item pending
-                    pend_u = cur.unit;
-                    pend_g = nstore;
-                }
-            }
             if (lane == 0 && warp < 16) TR(warp, ti, 32);
         }
         if (lane == 0) bulk_wait<0>();
-        if (counters) flush(true);
     }
     tc_fence_before();
     __syncthreads();

@@ -25,7 +25,7 @@ METRICS = [
 
 
 def short(name):
-    for k in ("tc_row_stage", "tc_column_stage", "tc_column_wide", "tc_alpha_r_stage", "tc_fused", "row_stage",
+    for k in ("tc_row_stage", "tc_column_stage", "tc_column_wide", "tc_alpha_r_stage", "tc_row_pair", "row_stage",
               "column_stage", "alpha_r_stage"):
         if k in name:
             return ("tc_" if name.find("tc_") >= 0 and not k.startswith("tc_") else "") + k
