@@ -18,7 +18,7 @@ import json,sys
 d=json.loads(sys.stdin.read()); d['args']='$a'; print(json.dumps(d))" >> gpurun_out/ev/sweep.jsonl
 done
 for spec in "sf 1" "sf3hw 1" "kv21 1" "sf 2"; do
-  set -- $spec; cfg=$1; it=$2; tag=r1c_${cfg}_t${it}
+  set -- $spec; cfg=$1; it=$2; tag=${TAG:-r1d}_${cfg}_t${it}
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tc_ --csv \
       --log-file gpurun_out/ev/${tag}_launches.csv python bench.py --config $cfg --iters $it --steps 5 --warmup 3 \
       --no-dense --no-cpu > gpurun_out/ev/${tag}_launches_bench.log 2>&1
