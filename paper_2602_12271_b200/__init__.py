@@ -38,6 +38,7 @@ __all__ = [
     "AttentionProblem", "SolverConfig", "SolverError", "SolverTrace", "MonarchFactors",
     "TiledMonarchFactors", "FactorError", "ShapeError", "solve", "solve_tiled",
     "attention_output", "monarch_attention",
+    "load_problem", "save_problem", "TensorFileError", "load_qkv", "FrameKVCache", "Rollout", "rollout_chunks",
 ]
 
 
@@ -51,4 +52,8 @@ def __getattr__(name):
     if name in ("SolverError", "monarch_attention"):
         from . import ops
         return getattr(ops, name)
+    if name in ("load_problem", "save_problem", "TensorFileError", "load_qkv", "FrameKVCache", "Rollout",
+                "rollout_chunks"):
+        from . import rollout
+        return getattr(rollout, name)
     raise AttributeError(name)
