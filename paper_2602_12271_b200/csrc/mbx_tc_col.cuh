@@ -93,8 +93,11 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_trigger();   // dependents may start their prologue once every CTA got here
-    pdl_wait();      // predecessor kernels (previous stage) complete and visible
+    // Dependents may start their prologue once every CTA got here.  The predecessor (the
+    // row stage) is waited for by the producer alone, right before its first workspace
+    // read: q columns are inputs the row stage does not write, and the row stage only
+    // triggers after its own wait, so they are already final.
+    pdl_trigger();
 
     auto decode = [&](int grp, int& bh, int& a, int& j0) {
         const int jg = grp % gpt;
@@ -161,6 +164,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 __syncwarp();
             }
             const int k0 = ch * kKC;
+            if (u == 0) pdl_wait();   // W and c_L of the row stage complete and visible
             for (int i = 0; i < 4; ++i) {   // aL_i + c_L_i
                 mbar_wait(&ring_empty[slot], sph ^ 1);
                 const int cb = i * 2 + (u & 1);

@@ -79,8 +79,9 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_trigger();   // dependents may start their prologue once every CTA got here
-    pdl_wait();      // predecessor kernels (previous stage) complete and visible
+    // dependents may start their prologue once every CTA got here; the producer alone waits
+    // for the row stage, after its first q-column load (q is final: see mbx_tc_col.cuh)
+    pdl_trigger();
 
     // item -> (column col, M tile mt); column -> (bh, a, j)
     auto decode = [&](int it, int& col, int& mt) {
@@ -111,6 +112,7 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
                 tma_load_4d(qd + 16384, &P.tqcw, &q_full[qb], 64, wcol, wrow, bh);
             }
             __syncwarp();
+            if (it == 0) pdl_wait();   // W and c_L of the row stage complete and visible
             for (int ch = 0; ch < nch; ++ch, ++u) {
                 const int k0 = ch * kWKC;
                 for (int part = 0; part < (outm ? 2 : 1); ++part, ++n) {   // aL, then Y

@@ -221,8 +221,8 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_trigger();   // dependents may start their prologue once every CTA got here
     pdl_wait();      // predecessor kernels (previous stage) complete and visible
+    pdl_trigger();   // only then may dependents start (they read q before their own wait)
 
 #define WAITX(bar, par) do { if (P.dbg & 64) mbar_spin(bar, par); else if (P.dbg & 128) mbar_wait_nohint(bar, par); else mbar_wait(bar, par); } while (0)
     RowCursor cur;

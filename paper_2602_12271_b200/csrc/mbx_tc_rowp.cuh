@@ -143,8 +143,8 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    pdl_trigger();
-    pdl_wait();
+    pdl_wait();      // predecessor kernels complete and visible
+    pdl_trigger();   // only then may dependents start (they read q before their own wait)
 
     PairCursor cur;
     cur.init(g, blockIdx.x, gridDim.x);
