@@ -37,7 +37,7 @@ __all__ = [
     "lower_square", "make_tile_plan", "phi_ordering", "rho_ordering",
     "AttentionProblem", "SolverConfig", "SolverError", "SolverTrace", "MonarchFactors",
     "TiledMonarchFactors", "FactorError", "ShapeError", "solve", "solve_tiled",
-    "attention_output", "monarch_attention",
+    "attention_output", "monarch_attention", "monarch_attention_host",
     "load_problem", "save_problem", "TensorFileError", "load_qkv", "FrameKVCache", "Rollout", "rollout_chunks",
 ]
 
@@ -49,7 +49,7 @@ def __getattr__(name):
                 "attention_output"):
         from . import solver
         return getattr(solver, name)
-    if name in ("SolverError", "monarch_attention"):
+    if name in ("SolverError", "monarch_attention", "monarch_attention_host"):
         from . import ops
         return getattr(ops, name)
     if name in ("load_problem", "save_problem", "TensorFileError", "load_qkv", "FrameKVCache", "Rollout",

@@ -278,3 +278,23 @@ def test_head_slices_of_single_batch_stay_on_tensor_cores(cuda):
     assert ops.selected_path(qs, ks, vs, low, 1) == "tcgen05"
     part = ops.forward(qs, ks, vs, low, 1)
     assert torch.equal(part, full[:, 1:3])
+
+
+@pytest.mark.parametrize("B,H,chunks,q_frames", [(1, 12, None, 3), (2, 3, 4, 3), (1, 2, 2, 1)])
+def test_host_api_pipelined_matches_device(cuda, B, H, chunks, q_frames):
+    """monarch_attention_host (pinned host tensors, H2D / forward / D2H pipelined over
+    (b,h) chunks on three streams) returns exactly the device call's output, for
+    square and chunked-KV problems."""
+    g = torch.Generator(device="cpu").manual_seed(B * 10 + H)
+    frames = 3
+    q = torch.randn(B, H, q_frames * 4680 // 3, 128, generator=g).to(torch.bfloat16).pin_memory()
+    k, v = (torch.randn(B, H, frames * 1560, 128, generator=g).to(torch.bfloat16).pin_memory() for _ in range(2))
+    plan = _sf_plan(frames)
+    kvf = frames if q_frames != frames else None
+    out = pk.monarch_attention_host(q, k, v, plan, kv_frames=kvf, chunks=chunks)
+    torch.cuda.synchronize()
+    ref = pk.monarch_attention(q.to(cuda), k.to(cuda), v.to(cuda), plan, kv_frames=kvf)
+    assert out.device.type == "cpu"
+    assert torch.equal(out, ref.cpu())
+    with pytest.raises(pk.SolverError):
+        pk.monarch_attention_host(q.to(cuda), k, v, plan)
