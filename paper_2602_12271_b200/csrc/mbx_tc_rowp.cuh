@@ -12,15 +12,18 @@
 //   MMA2  [aL | Y]_h = P_h . [K | V]_{c,k_h}   2 x 2 x (64 x 128 x 64), A = P in TMEM
 //   epilogue: warps 6-9 (aL) / 10-13 (Y), per warp two 16-row TMA stores (one per half)
 // (solver.py:187-191 R update and c_L; factors.py:123 Y = R V)
-constexpr int kPKV = 4;   // K/V ring stages (one key row each)
+constexpr int kPKV = 5;   // K/V ring stages (one key row each), at most
 constexpr int kPSB = 3;   // S/P buffers: MMA1 runs up to three tasks ahead of MMA2
 struct RowPSmem {
     static constexpr int kA = 0;                         // A slots [2] x [2 d-chunks][2 halves][64 rows][128 B]
     static constexpr int kASlot = 32768;
     static constexpr int kKV = 2 * kASlot;               // K/V rows [4] x [K c0 | K c1 | V c0 | V c1]
-    static constexpr int kKVBytes = 32768;
-    static constexpr int kStage = kKV + kPKV * kKVBytes; // staging [8 warps] x [32 rows][64] bf16
-    static constexpr int kBars = kStage + 8 * 4096;
+    // K/V ring: nkv stages of 4 chunks [K d0-63 | K d64-127 | V d0-63 | V d64-127], each
+    // chunk ceil(s2 / 8) x 8 rows of 128 B (7 KB at s2 = 52: five stages; 8 KB: four),
+    // then 1 KB of zeros that the last chunk's MMA reads of rows >= s2 may touch
+    static constexpr int kKVRegion = 5 * 4 * 7168 + 1024;
+    static constexpr int kStage = kKV + kKVRegion;       // staging [8 warps] x [16 rows][64] bf16
+    static constexpr int kBars = kStage + 8 * 2048;
     static constexpr int kNumBars = 4 + 2 * kPKV + 2 * kPSB + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
@@ -35,6 +38,7 @@ struct PairCursor {
     int t, t1, bh, kp, c, n_kp, gk, gq, nidx;
     int k0, q0, k1, q1;       // (row, query tile) of the two halves
     int kvi, kst, kph;        // K/V ring position of this task's first row
+    int nkv;                  // K/V ring stages
     bool valid;
     __device__ __forceinline__ void halves() {
         k0 = (2 * kp) / gq;
@@ -46,7 +50,8 @@ struct PairCursor {
             ++k1;
         }
     }
-    __device__ __forceinline__ void init(const Geometry& g, int cta, int ctas) {
+    __device__ __forceinline__ void init(const Geometry& g, int cta, int ctas, int stages) {
+        nkv = stages;
         gq = g.gq;
         nidx = g.gq * g.s1;
         n_kp = (nidx + 1) / 2;
@@ -70,7 +75,7 @@ struct PairCursor {
     __device__ __forceinline__ void advance() {
         for (int h = nrows(); h > 0; --h) {
             ++kvi;
-            if (++kst == kPKV) {
+            if (++kst == nkv) {
                 kst = 0;
                 kph ^= 1;
             }
@@ -96,8 +101,8 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RowPSmem::kBars);
     uint64_t* a_full = bars;                       // [2] A slot landed (Q per item, hat_alpha_R per task)
     uint64_t* a_empty = bars + 2;                  // [2] MMA1s done with it
-    uint64_t* kv_full = bars + 4;                  // [4]
-    uint64_t* kv_empty = kv_full + kPKV;           // [4]
+    uint64_t* kv_full = bars + 4;                  // [nkv]
+    uint64_t* kv_empty = kv_full + kPKV;           // [nkv]
     uint64_t* s_full = kv_empty + kPKV;            // [3]
     uint64_t* p_full = s_full + kPSB;              // [3]
     uint64_t* o_full = p_full + kPSB;              // [2]
@@ -106,6 +111,9 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     const int tid = threadIdx.x, lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
     const uint32_t box_bytes = (uint32_t)g.s2 * 128u;
+    const int cpitch = ((g.s2 + 7) / 8) * 1024;              // K/V chunk pitch (rows rounded to 8)
+    const int nkv = cpitch <= 7168 ? 5 : 4;                  // stages that fit the ring region
+    const int kvbytes = 4 * cpitch;
     const int ckey = ckey_stride(g);
     SPAN_AT(0, 0);
 
@@ -115,8 +123,6 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         tma_prefetch(&P.tv);
         tma_prefetch(&P.tws16);
         tma_prefetch(&P.tws16r);
-        tma_prefetch(&P.tws);
-        tma_prefetch(&P.tws_b);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
@@ -127,7 +133,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
         }
-        for (int i = 0; i < kPKV; ++i) {
+        for (int i = 0; i < nkv; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
         }
@@ -135,7 +141,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     }
     // K/V rows s2..63 and A rows s2..63 are never written by TMA: MMA2 multiplies K/V
     // padding by P = 0 (must be finite); A padding only feeds rows that are never stored.
-    for (int i = tid; i < kPKV * RowPSmem::kKVBytes / 16; i += blockDim.x)
+    for (int i = tid; i < RowPSmem::kKVRegion / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(smem + RowPSmem::kKV)[i] = make_uint4(0, 0, 0, 0);
     if (warp == 0) tmem_alloc<512>(tmem_slot);
     fence_proxy_async_smem();
@@ -147,7 +153,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     pdl_trigger();   // only then may dependents start (they read q before their own wait)
 
     PairCursor cur;
-    cur.init(g, blockIdx.x, gridDim.x);
+    cur.init(g, blockIdx.x, gridDim.x, nkv);
     const int t0 = cur.t;
     int ti = 0;   // trace event index (MBX_TRACE builds)
 
@@ -189,19 +195,20 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             int kvi = pc.kvi, kst = pc.kst, kph = pc.kph;
             for (int r = 0; r < pc.nrows(); ++r) {
                 mbar_wait(&kv_empty[kst], kph ^ 1);
-                const int tok = (int)row_base(g, false, pc.c, pc.kr(r));
+                // dbg 8 (timing only): every K/V load reads the same (L2-resident) row
+                const int tok = (P.dbg & 8) ? 0 : (int)row_base(g, false, pc.c, pc.kr(r));
                 if (leader) {
                     mbar_expect_tx(&kv_full[kst], 4u * box_bytes);
-                    uint8_t* kb = smem + RowPSmem::kKV + kst * RowPSmem::kKVBytes;
+                    uint8_t* kb = smem + RowPSmem::kKV + kst * kvbytes;
                     tma_load_4d(kb, &P.tk, &kv_full[kst], 0, tok, h, b);
-                    tma_load_4d(kb + 8192, &P.tk, &kv_full[kst], 64, tok, h, b);
-                    tma_load_4d(kb + 16384, &P.tv, &kv_full[kst], 0, tok, h, b);
-                    tma_load_4d(kb + 24576, &P.tv, &kv_full[kst], 64, tok, h, b);
+                    tma_load_4d(kb + cpitch, &P.tk, &kv_full[kst], 64, tok, h, b);
+                    tma_load_4d(kb + 2 * cpitch, &P.tv, &kv_full[kst], 0, tok, h, b);
+                    tma_load_4d(kb + 3 * cpitch, &P.tv, &kv_full[kst], 64, tok, h, b);
                 }
                 if (leader) TR(0, ti, 2);
                 __syncwarp();
                 ++kvi;
-                if (++kst == kPKV) {
+                if (++kst == nkv) {
                     kst = 0;
                     kph ^= 1;
                 }
@@ -236,15 +243,16 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     const uint32_t id = wide ? id2w : id2;
                     for (int hh = 0; hh < nm; ++hh) {
                         int kst = co.kst + (hh & two);
-                        if (kst >= kPKV) kst -= kPKV;
+                        if (kst >= nkv) kst -= nkv;
                         const uint32_t lane_h = (uint32_t)(hh * 16) << 16;
-                        const uint32_t b_lo = kv_lo + (uint32_t)kst * (RowPSmem::kKVBytes >> 4) + (8192u >> 4 << 16);
+                        // MN-major B: the two 64-wide d chunks of K (or V) are LBO = cpitch apart
+                        const uint32_t b_lo = kv_lo + (uint32_t)((kst * kvbytes) >> 4) + ((uint32_t)(cpitch >> 4) << 16);
                         const uint32_t pa = tmem + kPS + sb_o * 64 + lane_h;
                         for (int s = 0; s < (want_y ? 2 : 1); ++s) {
 #pragma unroll
                             for (int kk = 0; kk < 4; ++kk)
                                 mma_bf16_ts(tmem + (s ? kPOY : kPOA) + lane_h, pa + kk * 8,
-                                            desc(b_lo + ((s * 16384 + kk * 2048) >> 4)), id, kk > 0);
+                                            desc(b_lo + ((s * 2 * cpitch + kk * 2048) >> 4)), id, kk > 0);
                         }
                         if (hh == nm - 1 || two) mma_commit(&kv_empty[kst]);
                     }
@@ -267,7 +275,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 int kst = cs.kst, kph = cs.kph;
                 for (int r = 0; r < cs.nrows() && ready; ++r) {
                     ready = mbar_test_uniform(&kv_full[kst], kph);
-                    if (++kst == kPKV) {
+                    if (++kst == nkv) {
                         kst = 0;
                         kph ^= 1;
                     }
@@ -283,14 +291,14 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                         const uint32_t id = wide ? id1w : id1;
                         for (int hh = 0; hh < nm; ++hh) {
                             int ks = cs.kst + (hh & two);
-                            if (ks >= kPKV) ks -= kPKV;
+                            if (ks >= nkv) ks -= nkv;
                             const uint32_t aa = a_lo + (uint32_t)sl * (RowPSmem::kASlot >> 4) + ((hh * 8192) >> 4);
-                            const uint32_t b_lo = kv_lo + (uint32_t)ks * (RowPSmem::kKVBytes >> 4) + (1u << 16);
+                            const uint32_t b_lo = kv_lo + (uint32_t)((ks * kvbytes) >> 4) + (1u << 16);
                             const uint32_t d = tmem + kPS + sb_s * 64 + ((uint32_t)(hh * 16) << 16);
 #pragma unroll
                             for (int kk = 0; kk < 8; ++kk)
                                 mma_bf16(d, desc(aa + (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)),
-                                         desc(b_lo + (((kk >> 2) * 8192 + (kk & 3) * 32) >> 4)), id, kk > 0);
+                                         desc(b_lo + (((kk >> 2) * cpitch + (kk & 3) * 32) >> 4)), id, kk > 0);
                         }
                         mma_commit(&s_full[sb_s]);
                         if (last_use) mma_commit(&a_empty[sl]);
@@ -352,7 +360,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             const float mb = m * sl2;
             float p[64];
 #pragma unroll
-            for (int i = 0; i < 64; ++i) p[i] = ex2(fmaf(z[i], sl2, -mb));
+            for (int i = 0; i < 64; ++i) p[i] = (P.dbg & 4) ? z[i] : ex2(fmaf(z[i], sl2, -mb));   // dbg 4: timing only
             float lq[8], aq[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
@@ -396,10 +404,8 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
         const int nr = min(16, g.s2 - quad * 16);             // M=64 pair: rows j of this warp per half
-        const CUtensorMap* map = nr == 16 ? &P.tws16 : &P.tws16r;
         const int nrw = min(32, g.s2 - 32 * (quad & 1));      // shared-row M=128: rows of half quad/2
-        const CUtensorMap* mapw = (quad & 1) ? &P.tws_b : &P.tws;
-        uint8_t* stg = smem + RowPSmem::kStage + (warp - 6) * 4096;
+        uint8_t* stg = smem + RowPSmem::kStage + (warp - 6) * 2048;   // 16 rows: one store at a time
         for (int t = 0; cur.valid; ++t, cur.advance()) {
             const int nh = cur.nh();
             const bool wide = nh == 2 && cur.nrows() == 1;
@@ -421,29 +427,41 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             tc_fence_before();
             mbar_arrive(&o_empty[set]);
             if (lane == 0) TR(warp, ti, 32);
-            if (store_ok) {
+            if (store_ok && !(P.dbg & 1)) {   // dbg 1: timing experiment without the workspace stores
+                // per part, two 16-row stores: M=64 pair -> lanes 0-15 / 16-31 are halves 0 / 1;
+                // shared-row M=128 -> lanes 0-15 / 16-31 are rows j0 .. j0+15 / j0+16 .. of half quad/2
 #pragma unroll
                 for (int part = 0; part < 2; ++part) {
-                    if (lane == 0) bulk_wait_read<0>();
-                    __syncwarp();
-                    const uint32_t srow = smem_u32(stg) + lane * 128;
 #pragma unroll
-                    for (int cc = 0; cc < 8; ++cc)
-                        st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pk[part][4 * cc], pk[part][4 * cc + 1],
-                                     pk[part][4 * cc + 2], pk[part][4 * cc + 3]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (wide) {   // staging rows = j 32 (quad % 2) .. of half quad / 2
+                    for (int sub = 0; sub < 2; ++sub) {
+                        int rows, key, col;
+                        if (wide) {
                             const int hw = quad >> 1;
-                            tma_store_4d_hint(mapw, stg, 0, cur.c * g.s1 + cur.kr(hw), 2 * set + part,
-                                              (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1), w_policy);
+                            rows = min(16, nrw - 16 * sub);
+                            key = cur.c * g.s1 + cur.kr(hw);
+                            col = (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1) + 16 * sub;
                         } else {
-                            for (int hh = 0; hh < nh; ++hh)   // rows 16 hh .. of the staging: half hh (key row k_hh)
-                                tma_store_4d_hint(map, stg + hh * 2048, 0, cur.c * g.s1 + cur.kr(hh), 2 * set + part,
-                                                  col0 + cur.qt(hh) * g.s2, w_policy);
+                            rows = sub < nh ? nr : 0;
+                            key = cur.c * g.s1 + cur.kr(sub);
+                            col = col0 + cur.qt(sub) * g.s2;
                         }
-                        bulk_commit();
+                        if (rows <= 0) continue;
+                        if (lane == 0) bulk_wait_read<0>();
+                        __syncwarp();
+                        if ((lane >> 4) == sub) {
+                            const uint32_t srow = smem_u32(stg) + (lane & 15) * 128;
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc)
+                                st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pk[part][4 * cc], pk[part][4 * cc + 1],
+                                             pk[part][4 * cc + 2], pk[part][4 * cc + 3]);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_4d_hint(rows == 16 ? &P.tws16 : &P.tws16r, stg, 0, key, 2 * set + part, col,
+                                              w_policy);
+                            bulk_commit();
+                        }
                     }
                 }
             }
