@@ -39,6 +39,8 @@ __all__ = [
     "TiledMonarchFactors", "FactorError", "ShapeError", "solve", "solve_tiled",
     "attention_output", "monarch_attention", "monarch_attention_host",
     "load_problem", "save_problem", "TensorFileError", "load_qkv", "FrameKVCache", "Rollout", "rollout_chunks",
+    "save_factors", "load_factors", "densify", "densify_tiled", "approx_attention_matrix", "objective",
+    "identity_factors", "frobenius_mse",
 ]
 
 
@@ -56,4 +58,8 @@ def __getattr__(name):
                 "rollout_chunks"):
         from . import rollout
         return getattr(rollout, name)
+    if name in ("save_factors", "load_factors", "densify", "densify_tiled", "approx_attention_matrix", "objective",
+                "identity_factors", "frobenius_mse"):
+        from . import verify
+        return getattr(verify, name)
     raise AttributeError(name)

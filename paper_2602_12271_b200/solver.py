@@ -15,9 +15,9 @@ Same names, argument meaning, return layout and error classes as
 
 The arithmetic runs on the GPU through the C ABI (fp32 for numpy inputs,
 bf16 for bfloat16 torch inputs); results come back as float64 numpy arrays
-like the reference's.  Verification-only features that materialise N x N
-matrices (trace_objective / trace_mse, keep_workspace) are out of scope and
-raise SolverError.
+like the reference's.  trace_objective / trace_mse (N <= 4096 verification
+paths) are recorded on the GPU by verify.solve_traced; keep_workspace (the
+solver's intermediate tensors) raises SolverError.
 """
 
 from __future__ import annotations
@@ -181,9 +181,9 @@ def _to_device(m, dtype=None) -> torch.Tensor:
 
 
 def _check_unsupported(solver: SolverConfig) -> None:
-    if solver.trace_objective or solver.trace_mse or solver.keep_workspace:
-        raise SolverError("trace_objective / trace_mse / keep_workspace densify N x N and are "
-                          "verification paths of the reference; they are out of scope here")
+    if solver.keep_workspace:
+        raise SolverError("keep_workspace exports the solver's intermediate tensors (alpha/beta/z of both "
+                          "stages); the fused kernels never materialise them")
 
 
 def _run(problem: AttentionProblem, low, solver: SolverConfig, want_output: bool):
@@ -202,10 +202,18 @@ def _host(t: torch.Tensor) -> np.ndarray:
 
 def solve(problem: AttentionProblem, config: BlockConfig,
           solver: SolverConfig = SolverConfig()) -> tuple[MonarchFactors, SolverTrace]:
-    """Untiled factors under ``config`` (solver.py:114-158)."""
+    """Untiled factors under ``config`` (solver.py:114-158).  trace_objective /
+    trace_mse record per-refinement values on the GPU (verify.solve_traced)."""
     if config.shape != problem.shape:
         raise SolverError(f"config shape {config.shape} != problem shape {problem.shape}")
     _check_unsupported(solver)
+    if solver.trace_objective or solver.trace_mse:
+        from .verify import solve_traced
+        return solve_traced(problem, config, solver)
+    return _solve_untraced(problem, config, solver)
+
+
+def _solve_untraced(problem: AttentionProblem, config: BlockConfig, solver: SolverConfig):
     low = lower_square(config)
     _, lf, rf = _run(problem, low, solver, False)
     order = config.ordering().to_phi()
@@ -215,10 +223,17 @@ def solve(problem: AttentionProblem, config: BlockConfig,
 
 def solve_tiled(problem: AttentionProblem, plan: TilePlan,
                 solver: SolverConfig = SolverConfig()) -> tuple[TiledMonarchFactors, SolverTrace]:
-    """Tiled factors for ``plan`` (solver.py:161-204)."""
+    """Tiled factors for ``plan`` (solver.py:161-204); traces as in ``solve``."""
     if plan.shape != problem.shape:
         raise SolverError(f"plan shape {plan.shape} != problem shape {problem.shape}")
     _check_unsupported(solver)
+    if solver.trace_objective or solver.trace_mse:
+        from .verify import solve_traced
+        return solve_traced(problem, plan, solver)
+    return _solve_tiled_untraced(problem, plan, solver)
+
+
+def _solve_tiled_untraced(problem: AttentionProblem, plan: TilePlan, solver: SolverConfig):
     low = lower_square(plan)
     _, lf, rf = _run(problem, low, solver, False)
     order = plan.ordering().to_phi()

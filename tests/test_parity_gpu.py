@@ -91,7 +91,9 @@ def test_solver_errors_match_reference(cuda):
     with pytest.raises(pk.SolverError):
         pk.solve(problem, pk.aligned_config(pk.VideoShape(1, 3, 6), ("f", "h")))
     with pytest.raises(pk.SolverError):
-        pk.solve(problem, pk.aligned_config(s, ("f", "h")), pk.SolverConfig(trace_mse=True))
+        pk.solve(problem, pk.aligned_config(s, ("f", "h")), pk.SolverConfig(keep_workspace=True))
+    _, trace = pk.solve(problem, pk.aligned_config(s, ("f", "h")), pk.SolverConfig(iterations=2, trace_mse=True))
+    assert len(trace.mses) == 2 and not trace.objectives
     with pytest.raises(pk.ShapeError):
         fac, _ = pk.solve(problem, pk.aligned_config(s, ("f", "h")))
         pk.attention_output(fac, q[:5])
