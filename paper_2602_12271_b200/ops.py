@@ -213,6 +213,7 @@ def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = 
 
 
 _D2H_STREAMS: dict = {}
+_HOST_BUFS: dict = {}
 
 
 def _d2h_stream(device: torch.device) -> torch.cuda.Stream:
@@ -253,8 +254,17 @@ def monarch_attention_host(q, k, v, plan, iterations: int = 1, scale: float | No
     n = max(1, min(bh, chunks or 2))
     comp = torch.cuda.current_stream(dev)
     s_out = _d2h_stream(dev)
-    qd, kd, vd = (torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (qh, kh, vh))
-    od = torch.empty(oh.shape, dtype=oh.dtype, device=dev)
+    # device staging buffers are cached per shape: reuse is ordered by the current stream
+    # (this call's copies and forwards follow the previous call's, whose copy-out the
+    # current stream waited for), and the caching allocator never sees a cross-stream free
+    key = (dev.index, qh.shape, kh.shape, vh.shape, oh.shape, q.dtype, v.dtype)
+    bufs = _HOST_BUFS.get(key)
+    if bufs is None:
+        bufs = tuple(torch.empty(x.shape, dtype=x.dtype, device=dev) for x in (qh, kh, vh, oh))
+        if len(_HOST_BUFS) >= 4:
+            _HOST_BUFS.clear()
+        _HOST_BUFS[key] = bufs
+    qd, kd, vd, od = bufs
     for i in range(n):
         lo, hi = bh * i // n, bh * (i + 1) // n
         for d_, h_ in ((qd, qh), (kd, kh), (vd, vh)):
@@ -265,7 +275,6 @@ def monarch_attention_host(q, k, v, plan, iterations: int = 1, scale: float | No
         with torch.cuda.stream(s_out):
             oh[:, lo:hi].copy_(od[:, lo:hi], non_blocking=True)
     comp.wait_stream(s_out)
-    od.record_stream(s_out)   # the output buffer is read on s_out after this call returns
     return out
 
 
