@@ -83,6 +83,7 @@ struct TcParams {
     int stats_pitch;                      // floats per column: [max x s1p | 1/sum x s1p]
     CUtensorMap tqcw, toutw;              // wide column stage: q columns (128 rows), output rows (32 x 64)
     CUtensorMap tws16, tws16r;            // paired row stage: workspace stores of 16 / (s2 % 16) columns
+    CUtensorMap tqa;                      // alpha_R stage: q columns, s1 rounded up to 32 rows
     __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
@@ -292,7 +293,9 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         cuuint32_t qbox[4] = {64, 1, 128, 1};
         cuuint64_t ostr[3] = {(cuuint64_t)g.os[2] * 2, (cuuint64_t)g.os[2] * 2 * g.W, (cuuint64_t)g.os[1] * 2};
         cuuint32_t obox[4] = {64, 1, 32, 1};
+        cuuint32_t qabox[4] = {64, 1, (cuuint32_t)(((g.s1 + 31) / 32) * 32 < 128 ? ((g.s1 + 31) / 32) * 32 : 128), 1};
         if (!encode(&P.tqcw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !encode(&P.tqa, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qabox, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !encode(&P.toutw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, ostr, obox, CU_TENSOR_MAP_SWIZZLE_128B))
             return TC_FAIL("tensor map / argument check");
     }

@@ -47,7 +47,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
     if (tid == 0) {
         tma_prefetch(&P.tw128);
         tma_prefetch(&P.tc128);
-        tma_prefetch(&P.tqcw);
+        tma_prefetch(&P.tqa);
         tma_prefetch(&P.tar_st);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&ld_full[i], 1);
@@ -89,11 +89,12 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
             if (leader) {
                 uint8_t* base = smem + b * AlphaSmem::kBuf;
-                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * 128u * 128u + kAKC * 4u);
+                // q columns: s1p rows only (MMA1's N and MMA2's K stop there)
+                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * (uint32_t)s1p * 128u + kAKC * 4u);
                 tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
                 tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
-                tma_load_4d(base + AlphaSmem::kQc, &P.tqcw, &ld_full[b], 0, wcol, wrow, bh);
-                tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqcw, &ld_full[b], 64, wcol, wrow, bh);
+                tma_load_4d(base + AlphaSmem::kQc, &P.tqa, &ld_full[b], 0, wcol, wrow, bh);
+                tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqa, &ld_full[b], 64, wcol, wrow, bh);
                 tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
             }
             __syncwarp();
