@@ -300,3 +300,22 @@ def test_host_api_pipelined_matches_device(cuda, B, H, chunks, q_frames):
     assert torch.equal(out, ref.cpu())
     with pytest.raises(pk.SolverError):
         pk.monarch_attention_host(q.to(cuda), k, v, plan)
+
+
+@pytest.mark.parametrize("env", [{"MBX_PDL": "0"}, {"MBX_L2HINT": "0"}, {"MBX_WIDE": "1"}])
+def test_diagnostic_switches_keep_results(cuda, monkeypatch, env):
+    """The diagnostic switches (no programmatic dependent launch, no L2 residency
+    hints, the FlashAttention-style column stage forced on s1 <= 32) change
+    scheduling only: results stay within the bf16 budget of the oracle and, for
+    the first two, bitwise equal to the default launch sequence."""
+    g = torch.Generator(device="cpu").manual_seed(17)
+    q, k, v = (torch.randn(1, 2, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    low = pk.lower_square(_sf_plan())
+    ref = ops.forward(q, k, v, low, 2)
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    out = ops.forward(q, k, v, low, 2)
+    if "MBX_WIDE" in env:
+        assert orc.rel_l2(out.float().cpu().numpy(), _oracle_heads(q, k, v, low, 2)) < BF16_TOL
+    else:
+        assert torch.equal(out, ref)
