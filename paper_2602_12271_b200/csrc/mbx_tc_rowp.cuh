@@ -415,14 +415,20 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             if (lane == 0) TR(warp, ti, 31);
             tc_fence_after();
             uint32_t pk[2][32];
+            if (P.dbg & 2) {   // timing experiment: O released undrained (wrong results)
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t o[32];
-                tmem_ld32_nw(obuf + q4 * 32, o);
-                tmem_wait_ld();
+                for (int i = 0; i < 32; ++i) pk[0][i] = pk[1][i] = 0u;
+            } else {
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    pk[q4 >> 1][(q4 & 1) * 16 + i] = pack_bf16(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    uint32_t o[32];
+                    tmem_ld32_nw(obuf + q4 * 32, o);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        pk[q4 >> 1][(q4 & 1) * 16 + i] =
+                            pack_bf16(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
+                }
             }
             tc_fence_before();
             mbar_arrive(&o_empty[set]);
