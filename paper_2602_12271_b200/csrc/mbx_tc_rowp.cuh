@@ -360,7 +360,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             const float mb = m * sl2;
             float p[64];
 #pragma unroll
-            for (int i = 0; i < 64; ++i) p[i] = (P.dbg & 4) ? z[i] : ex2(fmaf(z[i], sl2, -mb));   // dbg 4: timing only
+            for (int i = 0; i < 64; ++i) p[i] = ex2(fmaf(z[i], sl2, -mb));
             float lq[8], aq[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
