@@ -16,6 +16,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
+
 namespace mbx {
 namespace {
 
@@ -235,7 +237,7 @@ bool tc_supported(const Geometry& g, int dtype, int flags) {
     return why == nullptr;
 }
 
-size_t tc_workspace_bytes(const Geometry& g) {
+static size_t tc_workspace_one(const Geometry& g) {
     const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
     size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4);
     if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 2 * ((g.s1 + 31) / 32) * 32 * 4);
@@ -249,8 +251,8 @@ static cudaError_t tc_fail(const char* what, int line) {
 }
 #define TC_FAIL(what) tc_fail(what, __LINE__)
 
-cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
-                       void* workspace, cudaStream_t stream) {
+static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
+                                  void* workspace, cudaStream_t stream) {
     Geometry g = g0;
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return TC_FAIL("tensor map / argument check");
@@ -449,6 +451,67 @@ cudaError_t tc_forward(const Geometry& g0, const void* q, const void* k, const v
         }
     }
     return cudaGetLastError();
+}
+
+// Long problems run as two concurrent halves of the heads, one on the caller's stream and
+// one on a side stream (fork / join through events, CUDA-graph capturable): the second
+// half's launches fill the ramp-up and drain of the first's persistent grids (KV21: 303 ->
+// 279 us with CUDA graphs, scripts/exp_streams.py), while short problems lose to the
+// halved work per CTA (C2: 59 -> 68 us), hence the size threshold.  MBX_SPLIT=0/1 overrides.
+static bool tc_split(const Geometry& g) {
+    if (g.bh != g.heads || g.heads % 2) return false;   // one batch, even head count
+    const char* e = getenv("MBX_SPLIT");
+    if (e) return e[0] == '1';
+    return (size_t)g.bh * g.gq * g.s2 * g.nkeys >= ((size_t)600 << 10);   // workspace rows
+}
+static Geometry half_heads(const Geometry& g) {
+    Geometry h = g;
+    h.heads = g.heads / 2;
+    h.bh = g.bh / 2;
+    return h;
+}
+
+struct SideStream {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static std::mutex g_side_mu;
+
+size_t tc_workspace_bytes(const Geometry& g) {
+    if (tc_split(g)) return 2 * align256(tc_workspace_one(half_heads(g)));
+    return tc_workspace_one(g);
+}
+
+cudaError_t tc_forward(const Geometry& g, const void* q, const void* k, const void* v, void* out, void* workspace,
+                       cudaStream_t stream) {
+    if (!tc_split(g)) return tc_forward_one(g, q, k, v, out, workspace, stream);
+    const Geometry h = half_heads(g);
+    const size_t wsh = align256(tc_workspace_one(h));
+    auto at = [&](const void* p, const int64_t* st) {   // head h.heads of a bf16 tensor
+        return reinterpret_cast<const char*>(p) + (size_t)h.heads * (size_t)st[1] * 2;
+    };
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    static SideStream sides[64];
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    // one enqueue at a time per process: the fork / join events are shared
+    std::lock_guard<std::mutex> lock(g_side_mu);
+    SideStream& ss = sides[dev];
+    if (!ss.side) {
+        if ((e = cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming)) != cudaSuccess)
+            return e;
+    }
+    if ((e = cudaEventRecord(ss.fork, stream)) != cudaSuccess || (e = cudaStreamWaitEvent(ss.side, ss.fork, 0)) != cudaSuccess)
+        return e;
+    cudaError_t e1 = tc_forward_one(h, q, k, v, out, workspace, stream);
+    cudaError_t e2 = tc_forward_one(h, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
+                                    reinterpret_cast<char*>(workspace) + wsh, ss.side);
+    if ((e = cudaEventRecord(ss.join, ss.side)) != cudaSuccess || (e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess)
+        return e;
+    return e1 != cudaSuccess ? e1 : e2;
 }
 
 }  // namespace mbx

@@ -319,3 +319,22 @@ def test_diagnostic_switches_keep_results(cuda, monkeypatch, env):
         assert orc.rel_l2(out.float().cpu().numpy(), _oracle_heads(q, k, v, low, 2)) < BF16_TOL
     else:
         assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("q_frames,T", [(3, 1), (3, 2), (1, 1)])
+def test_head_split_concurrent_halves_bitwise(cuda, monkeypatch, q_frames, T):
+    """MBX_SPLIT=1 runs the two halves of the heads concurrently on the caller's stream
+    and a side stream (the default for long problems); the result is bitwise the
+    single-sequence one, square and chunked-KV."""
+    g = torch.Generator(device="cpu").manual_seed(23 + T + q_frames)
+    frames, h, w = 7, 30, 52
+    q = torch.randn(1, 4, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k, v = (torch.randn(1, 4, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(2))
+    plan = _sf_plan(frames, h, w)
+    low = pk.lower_chunked(plan, q_frames)
+    monkeypatch.setenv("MBX_SPLIT", "0")
+    ref = ops.forward(q, k, v, low, T)
+    monkeypatch.setenv("MBX_SPLIT", "1")
+    out = ops.forward(q, k, v, low, T)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
