@@ -457,16 +457,18 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
 // one on a side stream (fork / join through events, CUDA-graph capturable): the second
 // half's launches fill the ramp-up and drain of the first's persistent grids (KV21: 303 ->
 // 279 us with CUDA graphs, scripts/exp_streams.py), while short problems lose to the
-// halved work per CTA (C2: 59 -> 68 us), hence the size threshold.  MBX_SPLIT=0/1 overrides.
+// halved work per CTA (C2: 59 -> 68 us), hence the size threshold.  Halves are of the heads
+// for one batch, of the batch otherwise (even counts only).  MBX_SPLIT=0/1 overrides.
 static bool tc_split(const Geometry& g) {
-    if (g.bh != g.heads || g.heads % 2) return false;   // one batch, even head count
+    const int B = g.bh / g.heads;
+    if (B == 1 ? g.heads % 2 != 0 : B % 2 != 0) return false;   // halves of the heads (B = 1) or of the batch
     const char* e = getenv("MBX_SPLIT");
     if (e) return e[0] == '1';
     return (size_t)g.bh * g.gq * g.s2 * g.nkeys >= ((size_t)600 << 10);   // workspace rows
 }
-static Geometry half_heads(const Geometry& g) {
+static Geometry half_heads(const Geometry& g) {   // B = 1: first half of the heads; else of the batch
     Geometry h = g;
-    h.heads = g.heads / 2;
+    if (g.bh == g.heads) h.heads = g.heads / 2;
     h.bh = g.bh / 2;
     return h;
 }
@@ -487,8 +489,9 @@ cudaError_t tc_forward(const Geometry& g, const void* q, const void* k, const vo
     if (!tc_split(g)) return tc_forward_one(g, q, k, v, out, workspace, stream);
     const Geometry h = half_heads(g);
     const size_t wsh = align256(tc_workspace_one(h));
-    auto at = [&](const void* p, const int64_t* st) {   // head h.heads of a bf16 tensor
-        return reinterpret_cast<const char*>(p) + (size_t)h.heads * (size_t)st[1] * 2;
+    auto at = [&](const void* p, const int64_t* st) {   // start of the second half (bf16 elements)
+        const size_t off = g.bh == g.heads ? (size_t)h.heads * (size_t)st[1] : (size_t)(h.bh / h.heads) * (size_t)st[0];
+        return reinterpret_cast<const char*>(p) + off * 2;
     };
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);

@@ -338,3 +338,16 @@ def test_head_split_concurrent_halves_bitwise(cuda, monkeypatch, q_frames, T):
     out = ops.forward(q, k, v, low, T)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_batch_split_concurrent_halves_bitwise(cuda, monkeypatch):
+    """With B even the concurrent halves are halves of the batch (odd head count here)."""
+    g = torch.Generator(device="cpu").manual_seed(29)
+    q, k, v = (torch.randn(2, 3, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    low = pk.lower_square(_sf_plan())
+    monkeypatch.setenv("MBX_SPLIT", "0")
+    ref = ops.forward(q, k, v, low, 1)
+    monkeypatch.setenv("MBX_SPLIT", "1")
+    out = ops.forward(q, k, v, low, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
