@@ -351,3 +351,22 @@ def test_batch_split_concurrent_halves_bitwise(cuda, monkeypatch):
     out = ops.forward(q, k, v, low, 1)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_head_split_is_graph_capturable(cuda, monkeypatch):
+    """The side-stream fork / join of the concurrent halves records into a CUDA graph."""
+    monkeypatch.setenv("MBX_SPLIT", "1")
+    g = torch.Generator(device="cpu").manual_seed(31)
+    q, k, v = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    low = pk.lower_square(_sf_plan())
+    out = torch.empty_like(q)
+    ops.forward(q, k, v, low, 1, out=out)
+    torch.cuda.synchronize()
+    eager = out.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        ops.forward(q, k, v, low, 1, out=out)
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
