@@ -5,10 +5,22 @@
 
 A step is one tiled MonarchAttention forward over one synthetic layer of the
 configured workload (default C2: one Self-Forcing chunk, B=1 H=12 d=128,
-(f,h,w)=(3,30,52), (h,w)-tiled plan, T=1, bf16) on each rank (weak scaling:
-every GPU processes its own layer; layers are independent (b,h) problems, so
-there is no collective in the data path).  ``value`` is whole-job ms per
-layer = max-over-ranks device time per step / N.
+(f,h,w)=(3,30,52), (h,w)-tiled plan, T=1, bf16).  Multi-GPU runs partition the
+flattened (b,h) unit list with ``shard.head_shard`` (no
+collective in the data path):
+
+* C2-C4 (``sf``, ``kv21``, ``n32k`` ...): weak scaling -- the job holds N
+  layers' worth of units (global batch N), each rank owns the contiguous span
+  of B*H units of one layer; ``value`` = whole-job ms per layer = max-over-ranks
+  device time per step / N.
+* C5 (``wan``): strong scaling of one fixed workload -- the Wan-1.3B-shaped
+  30-layer attention stack, B=8 H=12 N=32760, 96 (b,h) units split over the
+  ranks; ``value`` = ms per 30-layer stack (max over ranks).  The optional
+  NCCL all-gather of each layer's output shards (sequence-parallel DiT block)
+  is timed separately.
+
+``python bench.py --gpus N`` without a torchrun environment re-launches itself
+under ``torch.distributed.run`` with N ranks (127.0.0.1 rendezvous).
 
 Timing: W warm-up steps, then K steps timed with CUDA events on the launching
 stream; a 256 MB buffer is rewritten between steps to flush L2 (126 MB), and
@@ -53,9 +65,32 @@ CONFIGS = {
                  "C4c N=32760 untiled aligned (fh,w) = (630,52)"),
     "n32k_mis": (1, 12, 21, 21, 30, 52, 128, "mis", "bf16",
                  "C4d N=32760 untiled misaligned raw (b1,b2) = (1260,26)"),
+    "wan": (8, 12, 21, 21, 30, 52, 128, (1, 30, 52), "bf16",
+            "C5 Wan-1.3B-shaped attention stack: 30 layers x B=8 H=12 N=32760 (h,w)-tiled (s=0.95), "
+            "96 (b,h) units head-sharded over the ranks"),
+    "wan_3hw": (8, 12, 21, 21, 30, 52, 128, (3, 30, 52), "bf16",
+                "C5b Wan-1.3B-shaped attention stack: 30 layers x B=8 H=12 N=32760 (3h,w)-tiled (s=0.97), "
+                "96 (b,h) units head-sharded over the ranks"),
     "c1": (1, 2, 1, 1, 32, 32, 64, None, "fp32",
            "C1 CPU-reference config: B=1 H=2 N=1024 (32,32) untiled fp32"),
 }
+STACKS = {"wan": 30, "wan_3hw": 30}   # strong-scaled multi-layer workloads (layers per step)
+
+
+def job_config(name, world, iterations):
+    """The ``config`` dict both arms print (identical, so the driver can match them)."""
+    B, H, fkv, fq, h, w, d, nb, dt, desc = CONFIGS[name]
+    strong = name in STACKS
+    plan = {None: "untiled (fh,w)", "mis": "raw (1260,26)"}.get(nb, None) if not isinstance(nb, tuple) \
+        else f"neighborhoods {nb[0]}x{nb[1]}x{nb[2]}"
+    return {"workload": desc, "config": name, "B_per_layer": B, "H": H, "frames_q": fq, "frames_kv": fkv,
+            "h": h, "w": w, "d": d, "plan": plan, "iterations": iterations,
+            "layers_per_step": STACKS.get(name, world),
+            "global_batch": B if strong else B * world,
+            "units_per_step": B * H * STACKS.get(name, world),
+            "parallelism": f"(b,h) head shards over {world} rank(s), no data-path collective",
+            "scaling": "strong" if strong else "weak",
+            "l2": "flushed between timed steps (256 MB rewrite, outside events)"}
 
 
 def _peaks():
@@ -221,16 +256,17 @@ def dense_baselines(wl, q, k, v, steps, warmup, flush, stream):
 # reference CPU arm
 # --------------------------------------------------------------------------
 
-def _ref_worker(args):
-    """One (b,h) unit through the unmodified reference (or the oracle port)."""
+_CPU = {}   # job description + pre-generated inputs, inherited by the forked pool workers
+
+
+def _cpu_unit(i):
+    """One (b,h) unit through the unmodified reference (or the oracle port); returns seconds.
+    Inputs were generated before the pool was forked (outside every timed region)."""
     import numpy as np
 
-    kind, cfg_name, T, seed = args
-    wl = workload(cfg_name, T)
-    rng = np.random.default_rng(seed)
-    q = rng.standard_normal((wl["nq"], wl["d"])).astype(np.float32)
-    k = rng.standard_normal((wl["nk"], wl["d"])).astype(np.float32)
-    v = rng.standard_normal((wl["nk"], wl["dv"])).astype(np.float32)
+    kind, wl = _CPU["kind"], _CPU["wl"]
+    q, k, v = _CPU["inputs"][i % len(_CPU["inputs"])]
+    T = wl["T"]
     t0 = time.perf_counter()
     if kind == "reference":
         import monarchbench as mb
@@ -239,14 +275,16 @@ def _ref_worker(args):
         if wl["nb"] is None:
             cfg = mb.aligned_config(shape, ("f", "h"))
             fac, _ = mb.solve(mb.AttentionProblem(q, k, v, shape), cfg, mb.SolverConfig(iterations=T))
-            mb.attention_output(fac, v)
+        elif wl["nb"] == "mis":
+            cfg = mb.config_from_sizes(shape, 1260, 26)
+            fac, _ = mb.solve(mb.AttentionProblem(q, k, v, shape), cfg, mb.SolverConfig(iterations=T))
         else:
             plan = mb.make_tile_plan(shape, mb.aligned_config(shape, ("f", "h")), wl["nb"])
             qq = q
             if wl["fq"] != wl["fkv"]:   # chunked-KV via the square embedding
                 qq = np.vstack([np.zeros((wl["nk"] - wl["nq"], wl["d"]), np.float32), q])
             fac, _ = mb.solve_tiled(mb.AttentionProblem(qq, k, v, shape), plan, mb.SolverConfig(iterations=T))
-            mb.attention_output(fac, v)
+        mb.attention_output(fac, v)
     else:
         from oracle import monarch_oracle as orc
 
@@ -266,22 +304,71 @@ def _ref_kind():
     return "port"
 
 
-def cpu_layer_ms(cfg_name, T, units, cores, kind, max_units=None):
-    """Wall ms to run `units` (b,h) problems over a process pool of `cores`."""
-    import multiprocessing as mp
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
 
-    n = units if max_units is None else min(units, max_units)
-    jobs = [(kind, cfg_name, T, 1000 + i) for i in range(n)]
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    if cores > 1:
-        with ctx.Pool(min(cores, n)) as pool:
-            pool.map(_ref_worker, jobs)
-    else:
-        for j in jobs:
-            _ref_worker(j)
-    wall = time.perf_counter() - t0
-    return wall * 1e3 * units / n, n
+    return platform.processor() or "unknown"
+
+
+class CpuArm:
+    """The reference CPU path on the host cores: inputs generated once, one process
+    pool forked once (both outside the timed regions); a timed "wave" runs one unit
+    per pool process concurrently."""
+
+    def __init__(self, cfg_name, T, cores):
+        import multiprocessing as mp
+        import numpy as np
+
+        _env_threads()
+        self.kind = _ref_kind()
+        self.wl = workload(cfg_name, T)
+        self.cores = cores
+        self.units = self.wl["B"] * self.wl["H"] * STACKS.get(cfg_name, 1)   # units of one step (1 rank)
+        self.wave = min(cores, self.units)
+        rng = np.random.default_rng(1000)
+        wl = self.wl
+        _CPU.update(kind=self.kind, wl=wl, inputs=[
+            (rng.standard_normal((wl["nq"], wl["d"])).astype(np.float32),
+             rng.standard_normal((wl["nk"], wl["d"])).astype(np.float32),
+             rng.standard_normal((wl["nk"], wl["dv"])).astype(np.float32)) for _ in range(min(self.wave, 4))])
+        self.pool = mp.get_context("fork").Pool(self.wave) if self.wave > 1 else None
+
+    def wave_s(self):
+        """Wall seconds for one wave of `wave` concurrent units."""
+        t0 = time.perf_counter()
+        if self.pool is not None:
+            self.pool.map(_cpu_unit, range(self.wave), chunksize=1)
+        else:
+            _cpu_unit(0)
+        return time.perf_counter() - t0
+
+    def step_ms(self):
+        """One step (all `units`) extrapolated from one timed wave: waves run back to back."""
+        waves = -(-self.units // self.wave)
+        return self.wave_s() * 1e3 * waves, waves
+
+    def serial_unit_ms(self):
+        return _cpu_unit(0) * 1e3
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+    def describe(self, waves):
+        full = waves == 1 and self.wave == self.units
+        what = (f"full step: {self.units} (b,h) units run concurrently on a pool of {self.wave} processes"
+                if full else
+                f"one wave of {self.wave} concurrent (b,h) units timed per step, x{waves} waves for the "
+                f"step's {self.units} units (extrapolated linearly)")
+        return what + "; numpy single-threaded per unit; inputs and pool created outside the timed region"
 
 
 def _env_threads():
@@ -290,28 +377,36 @@ def _env_threads():
 
 
 def run_reference(args):
-    _env_threads()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    wl = workload(args.config, args.iters)
-    kind = _ref_kind()
     cores = len(os.sched_getaffinity(0))
-    units = wl["B"] * wl["H"]
+    arm = CpuArm(args.config, args.iters, cores)
     for _ in range(args.warmup):
-        cpu_layer_ms(args.config, args.iters, units, cores, kind, max_units=min(units, cores))
-    times = [cpu_layer_ms(args.config, args.iters, units, cores, kind)[0] for _ in range(args.steps)]
+        arm.wave_s()
+    times, waves = [], 1
+    for _ in range(args.steps):
+        ms, waves = arm.step_ms()
+        times.append(ms)
+    serial = arm.serial_unit_ms()
+    arm.close()
     ms = sum(times) / len(times)
+    strong = args.config in STACKS
+    value = ms if strong else ms / 1   # one rank's step = one layer (weak) / the whole stack (strong)
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms/layer",
+        "impl": "reference", "metric": METRIC, "value": round(value, 3),
+        "unit": "ms/stack" if strong else "ms/layer",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": False, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic N(0,1) q/k/v (seeded)",
-        "config": {"workload": wl["desc"], "iterations": args.iters, "units_per_step": units},
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/layer", "cores": cores, "kind": kind,
-                         "sample": f"full layer ({units} (b,h) units) per step, process pool of {cores}, "
-                                   "numpy single-threaded per unit"},
-        "e2e": {"value": round(ms, 3), "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": job_config(args.config, world, args.iters),
+        "cpu_baseline": {"value": round(value, 3), "unit": "ms/stack" if strong else "ms/layer", "cores": arm.wave,
+                         "kind": arm.kind, "sample": arm.describe(waves), "cpu_model": _cpu_model(),
+                         "host_cores": cores, "serial_ms_per_unit_1core": round(serial, 2),
+                         "serial_ms_per_step_1core": round(serial * arm.units, 1)},
+        "e2e": {"value": round(value, 3), "unit": "ms/stack" if strong else "ms/layer",
+                "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -320,30 +415,104 @@ def run_reference(args):
 # our arm
 # --------------------------------------------------------------------------
 
+class _Dist:
+    """Barrier / max-reduce across ranks: NCCL when every rank has its own GPU, gloo
+    (host tensors) when ranks share a device (e.g. --gpus 2 on a one-GPU box)."""
+
+    def __init__(self, world, local):
+        import torch
+        import torch.distributed as dist
+
+        self.world = world
+        self.dist = dist
+        ndev = torch.cuda.device_count()
+        self.shared = world > ndev
+        self.device = torch.device("cuda", local % ndev)
+        self.backend = None
+        if world > 1:
+            self.backend = "gloo" if self.shared else "nccl"
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.device)
+            else:
+                dist.init_process_group("gloo")
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, x):
+        import torch
+
+        if self.world == 1:
+            return x
+        dev = self.device if self.backend == "nccl" else torch.device("cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.barrier()
+            self.dist.destroy_process_group()
+
+
+def _merge_stages(recs, steps):
+    """Per-stage device time per step from per-launch (name, start, ms) records: the
+    launches of one stage inside a step (e.g. the two concurrent halves on two
+    streams) are merged into one span [first start, last end] carrying the stage's
+    whole work, so shares and roofline use whole-stage work over whole-stage time."""
+    per_step = len(recs) // max(steps, 1)
+    stages = {}
+    for sidx in range(steps):
+        chunk = recs[sidx * per_step:(sidx + 1) * per_step]
+        spans = {}
+        for name, st, ms in chunk:
+            lo, hi, n = spans.get(name, (st, st + ms, 0))
+            spans[name] = (min(lo, st), max(hi, st + ms), n + 1)
+        for name, (lo, hi, n) in spans.items():
+            stages.setdefault(name, []).append((hi - lo, n))
+    out = []
+    for name, vals in stages.items():
+        out.append({"name": name, "ms_avg": round(sum(v for v, _ in vals) / len(vals), 5),
+                    "launches_per_step": sum(n for _, n in vals) / len(vals), "stage_spans_per_step": 1})
+    return out, per_step
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     import paper_2602_12271_b200 as pk
-    from paper_2602_12271_b200 import _lib, ops
+    from paper_2602_12271_b200 import _lib, ops, shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    D = _Dist(world, local)
+    torch.cuda.set_device(D.device)
+    dev = D.device
     stream = torch.cuda.current_stream(dev)
 
-    wl = workload(args.config, args.iters)
+    name = args.config
+    strong = name in STACKS
+    layers = STACKS.get(name, 1)
+    wl = workload(name, args.iters)
     dtype = torch.bfloat16 if wl["dtype"] == "bf16" else torch.float32
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
     B, H = wl["B"], wl["H"]
-    q = torch.randn(B, H, wl["nq"], wl["d"], device=dev, dtype=dtype, generator=g)
-    k = torch.randn(B, H, wl["nk"], wl["d"], device=dev, dtype=dtype, generator=g)
-    v = torch.randn(B, H, wl["nk"], wl["dv"], device=dev, dtype=dtype, generator=g)
-    out = torch.empty(B, H, wl["nq"], wl["dv"], device=dev, dtype=dtype)
+    # (b,h) units of the job: weak -> `world` layers of B*H units (rank r owns layer r);
+    # strong -> one B*H layer split over the ranks (each of the `layers` layers alike)
+    if strong:
+        start, stop = shard.head_shard(B, H, world, rank)
+    else:
+        start, stop = shard.head_shard(B * world, H, world, rank)
+    spans = [shard.head_shard(B, H, world, r) if strong else shard.head_shard(B * world, H, world, r)
+             for r in range(world)]
+    units = stop - start
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    # the rank's units as the heads of a size-1 batch (shard.local_slice layout)
+    q = torch.randn(1, units, wl["nq"], wl["d"], device=dev, dtype=dtype, generator=g)
+    k = torch.randn(1, units, wl["nk"], wl["d"], device=dev, dtype=dtype, generator=g)
+    v = torch.randn(1, units, wl["nk"], wl["dv"], device=dev, dtype=dtype, generator=g)
+    out = torch.empty(1, units, wl["nq"], wl["dv"], device=dev, dtype=dtype)
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def flush():
@@ -357,60 +526,59 @@ def run_ours(args):
     path = {0: "simt", 1: "tcgen05"}[lib.mbx_selected_path(prep.desc)]
     import ctypes
 
-    def step():
+    def layer():
         st = lib.mbx_forward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
                              out.data_ptr(), None, None, ws.data_ptr(), nbytes, stream.cuda_stream)
         if st != 0:
             _lib.check(st)
 
+    def step():
+        for _ in range(layers):
+            layer()
+
     # ---- timed region (device time, max over ranks) ----
     step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with ClockSampler(local) as clk:
+    D.barrier()
+    with ClockSampler(dev.index) as clk:
         total_ms = time_steps(step, args.steps, args.warmup, flush, stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    D.barrier()
+    total_ms = D.max(total_ms)
     ms_step = total_ms / args.steps
-    value = ms_step / world                      # whole-job ms per layer
+    value = ms_step if strong else ms_step / world   # ms per stack (strong) / whole-job ms per layer (weak)
+    ms_layer_local = ms_step / layers                # this rank's device time for one layer of its units
 
     # ---- per-kernel shares (same stream, L2 flushed, CUDA events per launch) ----
-    prof_steps = max(3, min(args.steps, 50))
+    prof_steps = max(3, min(args.steps, 20))
     lib.mbx_profile_enable(1)
     for _ in range(prof_steps):
         flush()
-        step()
+        layer()
+    torch.cuda.synchronize()
     lib.mbx_profile_enable(0)
-    recs = _lib.profile_collect()
-    per = {}
-    for name, ms in recs:
-        per.setdefault(name, []).append(ms)
-    launches_per_step = len(recs) / prof_steps
-    kernels = [{"name": n, "ms_avg": round(sum(v_) / len(v_), 5), "launches_per_step": len(v_) / prof_steps}
-               for n, v_ in per.items()]
+    recs = _lib.profile_collect_ex()
+    kernels, launches_per_layer = _merge_stages(recs, prof_steps)
     alg = algorithmic(wl)
+    alg_local = {kk: vv * units / (B * H) for kk, vv in alg.items()}   # this rank's share of one layer
     peaks = _peaks()
-    ksum = sum(kk["ms_avg"] * kk["launches_per_step"] for kk in kernels) or ms_step
+    ksum = sum(kk["ms_avg"] for kk in kernels) or ms_layer_local
     for kk in kernels:
-        kk["share"] = round(kk["ms_avg"] * kk["launches_per_step"] / ksum, 4)
-    dom = max(kernels, key=lambda kk: kk["ms_avg"] * kk["launches_per_step"]) if kernels else None
+        kk["share"] = round(kk["ms_avg"] / ksum, 4)
+    dom = max(kernels, key=lambda kk: kk["ms_avg"]) if kernels else None
     roofline = None
+    eb = 2 if dtype == torch.bfloat16 else 4
     if dom is not None:
-        name = dom["name"]
-        per_launch = 1.0 / max(dom["launches_per_step"], 1e-9)
-        if "row" in name:
-            flops = alg["row"] * per_launch
-            byts = (wl["B"] * wl["H"]) * (wl["nq"] * wl["d"] + wl["nk"] * (wl["d"] + wl["dv"])) * (2 if dtype == torch.bfloat16 else 4)
-        elif "column" in name:
-            flops = alg["col"] * per_launch
-            byts = (wl["B"] * wl["H"]) * (wl["nq"] * (wl["d"] + wl["dv"])) * (2 if dtype == torch.bfloat16 else 4)
+        kname = dom["name"]
+        if "row" in kname:
+            flops = alg_local["row"]
+            byts = units * (wl["nq"] * wl["d"] + wl["nk"] * (wl["d"] + wl["dv"])) * eb
+        elif "column" in kname:
+            flops = alg_local["col"]
+            byts = units * (wl["nq"] * (wl["d"] + wl["dv"])) * eb
         else:
-            flops, byts = alg["total"], alg["bytes"]
+            flops, byts = alg_local["total"], alg_local["bytes"]
+        per_launch_spans = 1
         t_s = dom["ms_avg"] * 1e-3
         t_tc = flops / (peaks["tc_burst"] * 1e12)
         t_hbm = byts / (peaks["hbm"] * 1e9)
@@ -422,77 +590,131 @@ def run_ours(args):
             ach = byts / t_s / 1e9
             roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"],
                         "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4)}
-        roofline.update({"kernel": name, "traffic": _ncu_traffic(name, args.config),
+        roofline.update({"kernel": kname, "traffic": _ncu_traffic(kname, name),
                          "peak_source": f"{peaks['src']} (MEASURED_PEAKS.json burst)",
-                         "algorithmic_flops_per_launch": int(flops), "algorithmic_bytes_per_launch": int(byts)})
+                         "algorithmic_flops_per_launch": int(flops), "algorithmic_bytes_per_launch": int(byts),
+                         "launches_merged": dom["launches_per_step"], "spans": per_launch_spans})
+
+    # ---- eager per-call latency through the public API (device tensors, no L2 flush) ----
+    eager = None
+    if not strong:
+        plan = wl["plan"]
+        kvf = wl["fkv"] if wl["fq"] != wl["fkv"] else None
+        o2 = torch.empty_like(out)
+        for _ in range(5):
+            pk.monarch_attention(q, k, v, plan, iterations=wl["T"], kv_frames=kvf, out=o2)
+        torch.cuda.synchronize()
+        n_calls = 200
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(n_calls):
+            pk.monarch_attention(q, k, v, plan, iterations=wl["T"], kv_frames=kvf, out=o2)
+        t1 = time.perf_counter()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        dev_ms = e0.elapsed_time(e1) / n_calls
+        eager = {"host_enqueue_us_per_call": round((t1 - t0) * 1e6 / n_calls, 2),
+                 "wall_us_per_call": round((t2 - t0) * 1e6 / n_calls, 2),
+                 "device_us_per_call_hot_l2": round(dev_ms * 1e3, 2),
+                 "overhead_us_above_device": round(max(0.0, (t2 - t0) * 1e6 / n_calls - dev_ms * 1e3), 2),
+                 "calls": n_calls, "api": "paper_2602_12271_b200.monarch_attention (device tensors)"}
 
     # ---- end-to-end through the public API with host buffers ----
     # monarch_attention_host: pinned host q/k/v in, host output back, H2D / forward / D2H
-    # pipelined over (b,h) chunks on three streams (all inside the timed region)
+    # pipelined over (b,h) chunks (all inside the timed region), once per layer of the step
     pin = [x.cpu().pin_memory() for x in (q, k, v)]
     out_h = torch.empty(out.shape, dtype=dtype).pin_memory()
     plan = wl["plan"]
     kvf = wl["fkv"] if wl["fq"] != wl["fkv"] else None
 
     def e2e_step():
-        pk.monarch_attention_host(pin[0], pin[1], pin[2], plan, iterations=wl["T"], kv_frames=kvf, out=out_h)
+        for _ in range(layers):
+            pk.monarch_attention_host(pin[0], pin[1], pin[2], plan, iterations=wl["T"], kv_frames=kvf, out=out_h)
 
-    e2e_total = time_steps(e2e_step, args.steps, args.warmup, flush, stream)
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    e2e_ms = e2e_total / args.steps / world
-    eb = 2 if dtype == torch.bfloat16 else 4
-    h2d = sum(x.numel() for x in pin) * eb
-    d2h = out_h.numel() * eb
+    e2e_steps = args.steps if not strong else max(3, min(args.steps, 5))
+    D.barrier()
+    e2e_total = D.max(time_steps(e2e_step, e2e_steps, min(args.warmup, 3), flush, stream))
+    e2e_ms = e2e_total / e2e_steps
+    e2e_value = e2e_ms if strong else e2e_ms / world
+    h2d = sum(x.numel() for x in pin) * eb * layers
+    d2h = out_h.numel() * eb * layers
 
-    # ---- dense attention on the same shape ----
+    # ---- optional NCCL all-gather of the output shards (sequence-parallel DiT block) ----
+    allgather = None
+    if strong and world > 1 and D.backend == "nccl":
+        def gather_step():
+            for _ in range(layers):
+                shard.all_gather_heads(out, B, H)
+
+        gather_step()
+        torch.cuda.synchronize()
+        D.barrier()
+        ag = D.max(time_steps(gather_step, max(3, min(args.steps, 10)), 2, flush, stream))
+        ag_steps = max(3, min(args.steps, 10))
+        allgather = {"ms_per_step": round(ag / ag_steps, 4), "ms_per_layer": round(ag / ag_steps / layers, 4),
+                     "bytes_per_rank_per_layer": int(out.numel() * eb), "backend": "nccl",
+                     "communicator_size": world}
+
+    # ---- dense attention on the same (local) shape ----
     dense = {}
     if not args.no_dense and rank == 0:
-        dense = dense_baselines(wl, q, k, v, args.steps, args.warmup, flush, stream)
+        dense = dense_baselines(wl, q, k, v, max(3, min(args.steps, 20)), args.warmup, flush, stream)
     dense_nums = {kname: val for kname, val in dense.items() if isinstance(val, float)}
-    best_dense = min(dense_nums.values()) if dense_nums else None
+    best_dense = min(dense_nums.values()) if dense_nums else None   # ms per layer of the local units
 
     # ---- CPU baseline (rank 0, N=1 only; bounded sample) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        _env_threads()
-        kind = _ref_kind()
         cores = len(os.sched_getaffinity(0))
-        units = wl["B"] * wl["H"]
-        sample_units = min(units, max(cores, 2))
-        ms_cpu, n_done = cpu_layer_ms(args.config, wl["T"], units, cores, kind, max_units=sample_units)
-        cpu = {"value": round(ms_cpu, 2), "unit": "ms/layer", "cores": min(cores, n_done), "kind": kind,
-               "sample": f"{n_done} of {units} (b,h) units of one layer over a pool of "
-                         f"{min(cores, n_done)} processes, extrapolated linearly to {units} units"}
+        arm = CpuArm(name, wl["T"], cores)
+        arm.wave_s()   # warm-up (imports, page faults)
+        ms_cpu, waves = arm.step_ms()
+        serial = arm.serial_unit_ms()
+        arm.close()
+        cpu = {"value": round(ms_cpu, 2), "unit": "ms/stack" if strong else "ms/layer", "cores": arm.wave,
+               "kind": arm.kind, "sample": arm.describe(waves), "cpu_model": _cpu_model(), "host_cores": cores,
+               "serial_ms_per_unit_1core": round(serial, 2), "serial_ms_per_step_1core": round(serial * arm.units, 1)}
 
     if rank == 0:
+        unit = "ms/stack" if strong else "ms/layer"
         line = {
-            "metric": METRIC, "value": round(value, 5), "unit": "ms/layer", "n_gpus": world,
+            "metric": METRIC, "value": round(value, 5), "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": False, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": wl["dtype"], "data": "synthetic N(0,1) q/k/v generated on device (seeded)",
-            "config": {"workload": wl["desc"], "B": B, "H": H, "frames_q": wl["fq"], "frames_kv": wl["fkv"],
-                       "h": wl["h"], "w": wl["w"], "d": wl["d"], "plan": plan.descriptor(),
-                       "iterations": wl["T"], "layers_per_rank_per_step": 1, "parallelism": f"dp{world} (b,h) shards",
-                       "l2": "flushed between timed steps (256 MB rewrite, outside events)", "path": path},
+            "config": job_config(name, world, wl["T"]),
+            "shards": {"units_per_rank": [b_ - a_ for a_, b_ in spans], "rank_spans": spans,
+                       "backend": D.backend, "shared_gpu": D.shared, "path": path,
+                       "plan": plan.descriptor() if hasattr(plan, "descriptor") else str(plan)},
             "dense_fa_ms": dense, "dense_fa_best_ms": best_dense,
-            "speedup_vs_dense": round(best_dense / ms_step, 3) if best_dense else None,
-            "effective_tflops": round(alg["total"] / (ms_step * 1e-3) / 1e12, 2),
-            "tc_util": round(alg["total"] / (ms_step * 1e-3) / 1e12 / peaks["tc_burst"], 4),
+            "speedup_vs_dense": round(best_dense / ms_layer_local, 3) if best_dense else None,
+            "effective_tflops": round(alg_local["total"] / (ms_layer_local * 1e-3) / 1e12 * world, 2),
+            "tc_util": round(alg_local["total"] / (ms_layer_local * 1e-3) / 1e12 / peaks["tc_burst"], 4),
             "algorithmic": {"flops_per_layer": alg["total"], "bytes_per_layer": alg["bytes"],
-                            "dense_flops_per_layer": alg["dense"]},
+                            "dense_flops_per_layer": alg["dense"], "rank0_units": units},
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_ms, 5), "unit": "ms/layer", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "e2e": {"value": round(e2e_value, 5), "unit": unit, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "api": "paper_2602_12271_b200.monarch_attention_host"},
+            "eager": eager, "allgather": allgather,
+            "gpu_launches": int(round(launches_per_layer * layers * args.steps)),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+    D.close()
+
+
+def _self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def _ncu_traffic(kernel, config):
@@ -518,6 +740,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

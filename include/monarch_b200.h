@@ -13,9 +13,22 @@
  *                           via attention_output                solver.py:207-217
  *
  * All pointers are DEVICE pointers owned by the caller (the library never
- * allocates or frees user memory).  All work is enqueued on `stream`
- * (a cudaStream_t passed as void*); no call synchronizes the device.
- * The descriptor is read during the call and not retained.
+ * allocates or frees user memory).  Work is enqueued on `stream` (a
+ * cudaStream_t passed as void*); no call synchronizes the device.  The
+ * descriptor is read during the call and not retained.
+ *
+ * Library-owned resources (process lifetime, created on first use):
+ *   - a cache of launch parameters (TMA tensor maps) keyed by the descriptor,
+ *     the pointers and the device, so repeated calls skip the host-side encode;
+ *   - for long tensor-core problems (see MBX_FLAG_SPLIT), one side stream and
+ *     a fork/join event pair PER (device, caller stream): half of the heads run
+ *     on the side stream, which first waits for an event recorded on `stream`
+ *     and on completion is joined back into `stream` by a second event.  All
+ *     work therefore stays ordered after everything previously enqueued on
+ *     `stream`, and everything later enqueued on `stream` runs after it.  The
+ *     fork/join is capturable: under stream capture the side stream joins the
+ *     caller's capture (the split is skipped if the side stream for that caller
+ *     stream does not exist yet, so no stream is created inside a capture).
  *
  * Errors: every entry point returns an mbx_status; a non-zero status leaves a
  * thread-local message readable with mbx_last_error().  The Python layer maps
@@ -56,6 +69,10 @@ typedef enum mbx_dtype {
 /* flags */
 #define MBX_FLAG_FORCE_GENERIC 0x1  /* route to the SIMT kernels even if a tensor-core path applies */
 #define MBX_FLAG_NO_OUTPUT 0x2      /* factors only (solve_tiled without attention_output)          */
+#define MBX_FLAG_FACTORS 0x4        /* the forward will export L' and R': size the workspace and pick
+                                       the path for it (mbx_workspace_bytes / mbx_selected_path)     */
+#define MBX_FLAG_NO_SPLIT 0x8       /* never run the concurrent head/batch halves                   */
+#define MBX_FLAG_SPLIT 0x10         /* always run the concurrent halves when the shape allows        */
 
 /*
  * One forward problem, batched over (batch, heads).  Tokens of a (b, h)
@@ -152,6 +169,21 @@ size_t mbx_apply_workspace_bytes(const mbx_desc* desc);
  */
 int mbx_profile_enable(int on);
 int mbx_profile_collect(float* ms, const char** names, int max_entries);
+/* Same, with each launch's start relative to the first recorded start (ms), so
+ * launches that overlap on different streams can be merged into one span. */
+int mbx_profile_collect_ex(float* start_ms, float* ms, const char** names, int max_entries);
+
+/*
+ * Process-wide diagnostic options (initialised from the environment variables
+ * of the same name on first use): "MBX_PDL" (programmatic dependent launch,
+ * default 1), "MBX_L2HINT" (L2 residency hints, 1), "MBX_PAIR" (row-stage
+ * variant, -1 auto / 0 classic / 1 half-packed), "MBX_WIDE" (wide column stage
+ * for s1 <= 32, 0), "MBX_SPLIT" (concurrent halves, -1 auto / 0 / 1),
+ * "MBX_DBG" (timing bits, results wrong), "MBX_VERBOSE".  Returns the previous
+ * value, or -1000 for an unknown name.  Not for use while another thread is
+ * enqueueing forwards.
+ */
+int mbx_set_option(const char* name, int value);
 
 #ifdef __cplusplus
 }

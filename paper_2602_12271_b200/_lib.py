@@ -17,12 +17,16 @@ ABI_VERSION = 1
 F32, BF16 = 0, 1
 FLAG_FORCE_GENERIC = 0x1
 FLAG_NO_OUTPUT = 0x2
+FLAG_FACTORS = 0x4
+FLAG_NO_SPLIT = 0x8
+FLAG_SPLIT = 0x10
 
 OK, BAD_SHAPE, BAD_PLAN, BAD_ITERS, BAD_EPS, BAD_DTYPE, NULL, WORKSPACE, UNSUPPORTED, CUDA = range(10)
 
 EXPORTS = ("mbx_version", "mbx_last_error", "mbx_validate", "mbx_workspace_bytes",
            "mbx_selected_path", "mbx_forward", "mbx_apply", "mbx_apply_workspace_bytes",
-           "mbx_profile_enable", "mbx_profile_collect", "mbx_token_index")
+           "mbx_profile_enable", "mbx_profile_collect", "mbx_profile_collect_ex", "mbx_token_index",
+           "mbx_set_option")
 
 
 class MbxDesc(ctypes.Structure):
@@ -95,6 +99,11 @@ def load() -> ctypes.CDLL:
     lib.mbx_profile_collect.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_char_p),
                                         ctypes.c_int]
     lib.mbx_profile_collect.restype = ctypes.c_int
+    lib.mbx_profile_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
+                                           ctypes.POINTER(ctypes.c_char_p), ctypes.c_int]
+    lib.mbx_profile_collect_ex.restype = ctypes.c_int
+    lib.mbx_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
+    lib.mbx_set_option.restype = ctypes.c_int
     if lib.mbx_version() != ABI_VERSION:
         raise ImportError(f"libmonarch_b200 ABI {lib.mbx_version()} != {ABI_VERSION}; rebuild")
     _lib = lib
@@ -108,8 +117,22 @@ def check(status: int) -> None:
 
 def profile_collect(max_entries: int = 4096) -> list[tuple[str, float]]:
     """Per-launch (kernel name, ms) recorded since profiling was enabled."""
+    return [(n, ms) for n, _, ms in profile_collect_ex(max_entries)]
+
+
+def profile_collect_ex(max_entries: int = 4096) -> list[tuple[str, float, float]]:
+    """Per-launch (kernel name, start ms relative to the first launch, ms)."""
     lib = load()
+    st = (ctypes.c_float * max_entries)()
     ms = (ctypes.c_float * max_entries)()
     names = (ctypes.c_char_p * max_entries)()
-    n = lib.mbx_profile_collect(ms, names, max_entries)
-    return [(names[i].decode(), float(ms[i])) for i in range(min(n, max_entries))]
+    n = lib.mbx_profile_collect_ex(st, ms, names, max_entries)
+    return [(names[i].decode(), float(st[i]), float(ms[i])) for i in range(min(n, max_entries))]
+
+
+def set_option(name: str, value: int) -> int:
+    """Process-wide diagnostic option (mbx_set_option); returns the previous value."""
+    prev = load().mbx_set_option(name.encode(), int(value))
+    if prev == -1000:
+        raise KeyError(name)
+    return prev

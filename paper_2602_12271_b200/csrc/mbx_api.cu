@@ -163,15 +163,23 @@ int mbx_profile_enable(int on) {
 }
 
 int mbx_profile_collect(float* ms, const char** names, int max_entries) {
+    return mbx_profile_collect_ex(nullptr, ms, names, max_entries);
+}
+
+int mbx_profile_collect_ex(float* start_ms, float* ms, const char** names, int max_entries) {
     const int n = (int)g_prof.size();
     for (int i = 0; i < n; ++i) {
         ProfRecord& r = g_prof[i];
         if (i < max_entries) {
-            float t = -1.f;
+            float t = -1.f, t0 = 0.f;
             if (cudaEventSynchronize(r.stop) == cudaSuccess) cudaEventElapsedTime(&t, r.start, r.stop);
+            if (start_ms && i > 0) cudaEventElapsedTime(&t0, g_prof[0].start, r.start);
             if (ms) ms[i] = t;
+            if (start_ms) start_ms[i] = t0;
             if (names) names[i] = r.name;
         }
+    }
+    for (ProfRecord& r : g_prof) {
         cudaEventDestroy(r.start);
         cudaEventDestroy(r.stop);
     }
@@ -180,6 +188,8 @@ int mbx_profile_collect(float* ms, const char** names, int max_entries) {
 }
 
 const char* mbx_last_error(void) { return g_last_error.c_str(); }
+
+int mbx_set_option(const char* name, int value) { return mbx::set_option(name, value); }
 
 int mbx_validate(const mbx_desc* desc) { return validate(desc, nullptr); }
 
@@ -198,13 +208,14 @@ int64_t mbx_token_index(const mbx_desc* desc, int is_query, int64_t slot) {
 int mbx_selected_path(const mbx_desc* desc) {
     mbx::Geometry g;
     if (validate(desc, &g) != MBX_OK) return -1;
-    return mbx::tc_supported(g, desc->dtype, desc->flags) ? 1 : 0;
+    return mbx::tc_supported(g, desc->dtype, desc->flags, (desc->flags & MBX_FLAG_FACTORS) != 0) ? 1 : 0;
 }
 
 size_t mbx_workspace_bytes(const mbx_desc* desc) {
     mbx::Geometry g;
     if (validate(desc, &g) != MBX_OK) return 0;
-    if (mbx::tc_supported(g, desc->dtype, desc->flags)) return mbx::tc_workspace_bytes(g);
+    if (mbx::tc_supported(g, desc->dtype, desc->flags, (desc->flags & MBX_FLAG_FACTORS) != 0))
+        return mbx::tc_workspace_bytes(g, desc->flags);
     return mbx::workspace_layout(g, nullptr, nullptr);
 }
 
@@ -218,13 +229,15 @@ int mbx_forward(const mbx_desc* desc, const void* q, const void* k, const void* 
     if (!q || !k || (want_out && (!v || !out)))
         return fail(MBX_ERR_NULL, "q, k, v and out must be non-NULL");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const bool tc = !l_factor && !r_factor && want_out && mbx::tc_supported(g, desc->dtype, desc->flags);
+    const bool factors = l_factor || r_factor;
+    const int flags = desc->flags | (factors ? MBX_FLAG_FACTORS : 0);
+    const bool tc = want_out && mbx::tc_supported(g, desc->dtype, flags, factors);
     cudaError_t e;
     if (tc) {
-        const size_t need = mbx::tc_workspace_bytes(g);
+        const size_t need = mbx::tc_workspace_bytes(g, flags);
         if (need && (!workspace || workspace_bytes < need))
             return fail(MBX_ERR_WORKSPACE, "workspace %zu < required %zu bytes", workspace_bytes, need);
-        e = mbx::tc_forward(g, q, k, v, out, workspace, s);
+        e = mbx::tc_forward(g, flags, q, k, v, out, l_factor, r_factor, workspace, s);
     } else {
         mbx::Workspace ws;
         const size_t need = mbx::workspace_layout(g, (char*)workspace, &ws);

@@ -71,10 +71,27 @@ cudaError_t generic_apply(const Geometry& g, int dtype, const float* l_factor,
                           const float* r_factor, const void* v, void* out,
                           const Workspace& ws, cudaStream_t stream);
 
+// Process-wide diagnostic options (mbx_set_option; initialised once from the
+// MBX_* environment variables).  -1 = automatic choice.
+struct Options {
+    int pdl = 1;        // programmatic dependent launch between stages
+    int l2hint = 1;     // W stores evict_last, last W reads evict_first
+    int dbg = 0;        // MBX_DBG timing bits (wrong results by construction)
+    int pair = -1;      // row stage: 0 classic, 1 half-packed
+    int wide = 0;       // 1: FlashAttention-style column stage for s1 <= 32 too (T = 1)
+    int split = -1;     // concurrent halves: 0 off, 1 on
+    int verbose = 0;    // print why a problem leaves the tcgen05 path / setup failures
+    unsigned version = 0;   // bumped on every change (keys the launch-parameter cache)
+};
+const Options& options();
+int set_option(const char* name, int value);
+
 // tcgen05 tensor-core kernels (mbx_tc.cu) -- bf16, contiguous tile rows.
-bool tc_supported(const Geometry& g, int dtype, int flags);
-size_t tc_workspace_bytes(const Geometry& g);
-cudaError_t tc_forward(const Geometry& g, const void* q, const void* k, const void* v,
-                       void* out, void* workspace, cudaStream_t stream);
+// `factors`: the call exports L' and R' (needs s1 <= 128 on this path).
+bool tc_supported(const Geometry& g, int dtype, int flags, bool factors);
+size_t tc_workspace_bytes(const Geometry& g, int flags);
+cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* k, const void* v,
+                       void* out, float* l_factor, float* r_factor, void* workspace,
+                       cudaStream_t stream);
 
 }  // namespace mbx

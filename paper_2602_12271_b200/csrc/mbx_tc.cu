@@ -1,10 +1,11 @@
 // tcgen05 / TMEM / TMA kernels of the tiled MonarchAttention forward (bf16,
-// d = d_v = 128, T = 1, tile rows of <= 64 tokens, <= 32 rows per tile,
-// <= 4 query tiles).  Two warp-specialized persistent kernels joined by a
-// bf16 workspace W[b,h,a,j,(c,k),0:256] = [aL | Y] and c_L (SURVEY.md
-// Appendix B):
-//   row stage    (mbx_tc_row.cuh)  solver.py:187-191, factors.py:123
-//   column stage (mbx_tc_col.cuh)  solver.py:192-195, factors.py:124
+// d = d_v = 128, tile rows of <= 64 tokens, any number of tiles, any T; T >= 2
+// and factor export need s1 <= 128).  Warp-specialized persistent kernels
+// joined by a bf16 workspace W[b,h,a,j,(c,k),0:256] = [aL | Y] and c_L
+// (SURVEY.md Appendix B):
+//   row stage    (mbx_tc_row.cuh, mbx_tc_rowp.cuh)  solver.py:187-191, factors.py:123
+//   column stage (mbx_tc_col.cuh, mbx_tc_colw.cuh)  solver.py:192-195, factors.py:124
+//   alpha_R hand-off / L export (mbx_tc_alpha.cuh)  solver.py:185-186
 // The plan's permutation is folded into TMA coordinates: each tile row is one
 // box at token row_base(tile, r); each tile column is one strided box.
 #include "mbx_internal.h"
@@ -90,10 +91,19 @@ struct TcParams {
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
     int l2hint;                           // W stores evict_last, last reads evict_first (MBX_L2HINT=0: off)
+    float* rfac;                          // optional R' export (fp32, factors.py:57-79 layout), last row stage
+    float* lfac;                          // optional L' export, written by the alpha kernel in mode 1
 };
 
 // Row-stage query groups (<= 3 query tiles each) of the classic row stage.
 __host__ __device__ __forceinline__ int row_groups(const Geometry& g) { return (g.gq + 2) / 3; }
+
+// One softmax row of the final R' (fp32, before the bf16 rounding the MMA operand gets).
+__device__ __forceinline__ void store_r_row(float* dst, const float* p, float inv_l, int s2) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i)
+        if (i < s2) dst[i] = p[i] * inv_l;
+}
 
 #include "mbx_tc_row.cuh"
 #include "mbx_tc_col.cuh"
@@ -172,15 +182,15 @@ bool make_qcol_map(CUtensorMap* m, const void* base, const Geometry& g, int nq) 
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+int num_sms(int dev) {   // per device (mixed-GPU hosts)
+    static int n[64] = {};
+    if (dev < 0 || dev >= 64) return 148;
+    if (!n[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        n[dev] = v > 0 ? v : 148;
     }
-    return n;
+    return n[dev];
 }
 
 bool strides_ok(const int64_t* s) {
@@ -201,19 +211,58 @@ bool column_grid(const Geometry& g, int* F, int* H, int* W) {
     return true;
 }
 
-bool pdl_enabled() {   // MBX_PDL=0 disables programmatic dependent launch
-    const char* e = getenv("MBX_PDL");
-    return !(e && e[0] == '0');
-}
-
 }  // namespace
 
+// ------------------------------------------------------------------ options
+static Options g_opts;
+static std::once_flag g_opts_once;
+static std::mutex g_opts_mu;
+
+static void init_options() {
+    auto env = [](const char* n, int dflt) {
+        const char* e = getenv(n);
+        return e && e[0] ? atoi(e) : dflt;
+    };
+    g_opts.pdl = env("MBX_PDL", 1);
+    g_opts.l2hint = env("MBX_L2HINT", 1);
+    g_opts.dbg = env("MBX_DBG", 0);
+    g_opts.pair = env("MBX_PAIR", -1);
+    g_opts.wide = env("MBX_WIDE", 0);
+    g_opts.split = env("MBX_SPLIT", -1);
+    g_opts.verbose = env("MBX_VERBOSE", 0);
+}
+
+const Options& options() {
+    std::call_once(g_opts_once, init_options);
+    return g_opts;
+}
+
+int set_option(const char* name, int value) {
+    std::call_once(g_opts_once, init_options);
+    if (!name) return -1000;
+    std::lock_guard<std::mutex> lock(g_opts_mu);
+    struct { const char* n; int* p; } tab[] = {
+        {"MBX_PDL", &g_opts.pdl}, {"MBX_L2HINT", &g_opts.l2hint}, {"MBX_DBG", &g_opts.dbg},
+        {"MBX_PAIR", &g_opts.pair}, {"MBX_WIDE", &g_opts.wide}, {"MBX_SPLIT", &g_opts.split},
+        {"MBX_VERBOSE", &g_opts.verbose}};
+    for (auto& t : tab)
+        if (strcmp(t.n, name) == 0) {
+            const int prev = *t.p;
+            *t.p = value;
+            ++g_opts.version;
+            return prev;
+        }
+    return -1000;
+}
+
 // Why a problem is not on the tcgen05 path (nullptr: it is); MBX_VERBOSE=1 prints it.
-static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags) {
+static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags, bool factors) {
     if (flags & MBX_FLAG_FORCE_GENERIC) return "forced generic";
+    if (flags & MBX_FLAG_NO_OUTPUT) return "factors without output";
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return "needs bf16 with d = dv = 128";
     if (g.s2 > kMaxS2) return "s2 > 64";
     if (g.T > 1 && g.s1 > 128) return "T > 1 with s1 > 128";   // alpha_R hand-off: query rows l on the MMA N axis
+    if (factors && g.s1 > 128) return "factor export with s1 > 128";   // L export shares the alpha_R kernel
     if (g.nf == 0 && (g.q_order || g.kv_order)) return "permuted plan without a closed form";
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return "tile rows are not contiguous grid rows";
@@ -228,31 +277,53 @@ static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags
     return nullptr;
 }
 
-bool tc_supported(const Geometry& g, int dtype, int flags) {
-    const char* why = tc_unsupported_reason(g, dtype, flags);
-    if (why && !(flags & MBX_FLAG_FORCE_GENERIC) && getenv("MBX_VERBOSE"))
+bool tc_supported(const Geometry& g, int dtype, int flags, bool factors) {
+    const char* why = tc_unsupported_reason(g, dtype, flags, factors);
+    if (why && !(flags & MBX_FLAG_FORCE_GENERIC) && options().verbose)
         fprintf(stderr, "mbx: tcgen05 path not used: %s (bh=%d heads=%d qs=%lld,%lld,%lld os=%lld,%lld,%lld)\n", why,
                 g.bh, g.heads, (long long)g.qs[0], (long long)g.qs[1], (long long)g.qs[2], (long long)g.os[0],
                 (long long)g.os[1], (long long)g.os[2]);
     return why == nullptr;
 }
 
-static size_t tc_workspace_one(const Geometry& g) {
-    const size_t rows = (size_t)g.bh * g.gq * g.s2 * g.nkeys;
-    size_t bytes = align256(rows * 512) + align256((size_t)g.bh * g.gq * g.s2 * ckey_stride(g) * 4);
-    if (g.T > 1) bytes += align256(rows * 256) + align256((size_t)g.bh * g.gq * g.s2 * 2 * ((g.s1 + 31) / 32) * 32 * 4);
-    return bytes;
+// Workspace of one launch sequence: W [col][part][key][64] bf16, c_L [col][ckey] f32,
+// L statistics [col][2 s1p] f32, and for T >= 2 hat_alpha_R [bh gq][key][j][128] bf16.
+struct TcLayout {
+    size_t w, wc, stats, ar, total;
+};
+static TcLayout tc_layout(const Geometry& g) {
+    const size_t ncols = (size_t)g.bh * g.gq * g.s2;
+    const size_t rows = ncols * g.nkeys;
+    const size_t s1p = ((g.s1 + 31) / 32) * 32;
+    TcLayout L;
+    L.w = 0;
+    L.wc = align256(rows * 512);
+    L.stats = L.wc + align256(ncols * ckey_stride(g) * 4);
+    L.ar = L.stats + align256(ncols * 2 * s1p * 4);
+    L.total = L.ar + (g.T > 1 ? align256(rows * 256) : 0);
+    return L;
 }
 
 // Failure of a host-side setup step: reported on stderr when MBX_VERBOSE is set.
 static cudaError_t tc_fail(const char* what, int line) {
-    if (getenv("MBX_VERBOSE")) fprintf(stderr, "mbx tc_forward: %s failed (mbx_tc.cu:%d)\n", what, line);
+    if (options().verbose) fprintf(stderr, "mbx tc_forward: %s failed (mbx_tc.cu:%d)\n", what, line);
     return cudaErrorInvalidValue;
 }
 #define TC_FAIL(what) tc_fail(what, __LINE__)
 
-static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
-                                  void* workspace, cudaStream_t stream) {
+// Everything one forward launch sequence needs, derived from the descriptor, the pointers
+// and the options; cached so repeated calls skip the tensor-map encodes.
+struct TcPlan {
+    TcParams P;
+    Geometry g;            // identity plans rewritten as a (1, s1, s2) neighborhood grid
+    bool pair, wide;
+    int grid_pair, grid_row, grid_col, grid_wide, grid_alpha;
+    int smem_row, smem_col, smem_pair, smem_wide, smem_alpha;
+};
+
+static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
+                              float* l_factor, float* r_factor, void* workspace, int dev, TcPlan* T) {
+    const Options& o = options();
     Geometry g = g0;
     int F, H, W;
     if (!column_grid(g, &F, &H, &W)) return TC_FAIL("tensor map / argument check");
@@ -260,52 +331,48 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
         g.F = F; g.H = H; g.W = W;
         g.nf = 1; g.nh = g.s1; g.nw = g.s2;
     }
+    const bool factors = l_factor || r_factor;
     const int B = g.bh / g.heads;
     const int nq = g.c1q * g.s1 * g.c2 * g.s2, nk = g.c1k * g.s1 * g.c2 * g.s2;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out | (uintptr_t)workspace) & 15)
         return TC_FAIL("tensor map / argument check");
-    TcParams P;
-    {
-        const char* e = getenv("MBX_DBG");
-        P.dbg = e ? atoi(e) : 0;
-        const char* h = getenv("MBX_L2HINT");
-        P.l2hint = h ? atoi(h) : 1;
-    }
+    TcParams& P = T->P;
+    memset(&P, 0, sizeof(P));
+    P.dbg = o.dbg;
+    P.l2hint = o.l2hint;
+    P.rfac = r_factor;
+    P.lfac = l_factor;
     if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, g.s2) ||
         !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&P.tqc, q, g, nq) ||
         !make_outcol_map(&P.tout, out, g, nq))
         return TC_FAIL("tensor map / argument check");
     const int64_t ncols = (int64_t)g.bh * g.gq * g.s2;
     const int64_t rows = ncols * g.nkeys;
-    __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(workspace);
-    float* Wc = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + align256(rows * 512));
+    const TcLayout lay = tc_layout(g);
+    char* wsb = reinterpret_cast<char*>(workspace);
+    __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(wsb + lay.w);
+    float* Wc = reinterpret_cast<float*>(wsb + lay.wc);
     P.wc = Wc;
     P.w = Wp;
-    P.stats = nullptr;
     const int s1p = ((g.s1 + 31) / 32) * 32;
+    P.stats = reinterpret_cast<float*>(wsb + lay.stats);
     P.stats_pitch = 2 * s1p;
     P.out = reinterpret_cast<__nv_bfloat16*>(out);
     P.out_bh_stride = g.os[1];
     P.out_tok_stride = g.os[2];
-    const char* wide_env = getenv("MBX_WIDE");   // 1: FlashAttention-style column stage for any s1 (experiments)
-    const bool wide = g.s1 > kMaxS1 || (g.T == 1 && wide_env && wide_env[0] == '1');
-    if (wide || g.T > 1) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
+    const bool wide = g.s1 > kMaxS1 || (g.T == 1 && o.wide == 1);
+    const bool stats = g.T > 1 || factors;   // statistics pass + alpha kernel (hand-off / L export)
+    if (wide || stats) {   // q columns of up to 128 rows; output rows of one warp (32 rows x 64 values)
         cuuint64_t dims[4] = {(cuuint64_t)kD, (cuuint64_t)g.W, (cuuint64_t)(nq / g.W), (cuuint64_t)g.bh};
         cuuint64_t qstr[3] = {(cuuint64_t)g.qs[2] * 2, (cuuint64_t)g.qs[2] * 2 * g.W, (cuuint64_t)g.qs[1] * 2};
         cuuint32_t qbox[4] = {64, 1, 128, 1};
         cuuint64_t ostr[3] = {(cuuint64_t)g.os[2] * 2, (cuuint64_t)g.os[2] * 2 * g.W, (cuuint64_t)g.os[1] * 2};
         cuuint32_t obox[4] = {64, 1, 32, 1};
-        cuuint32_t qabox[4] = {64, 1, (cuuint32_t)(((g.s1 + 31) / 32) * 32 < 128 ? ((g.s1 + 31) / 32) * 32 : 128), 1};
+        cuuint32_t qabox[4] = {64, 1, (cuuint32_t)(s1p < 128 ? s1p : 128), 1};
         if (!encode(&P.tqcw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !encode(&P.tqa, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, q, dims, qstr, qabox, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !encode(&P.toutw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, out, dims, ostr, obox, CU_TENSOR_MAP_SWIZZLE_128B))
             return TC_FAIL("tensor map / argument check");
-    }
-    __nv_bfloat16* AR = nullptr;
-    if (g.T > 1) {
-        char* after = reinterpret_cast<char*>(Wc) + align256((size_t)ncols * ckey_stride(g) * 4);
-        AR = reinterpret_cast<__nv_bfloat16*>(after);
-        P.stats = reinterpret_cast<float*>(after + align256((size_t)rows * 256));
     }
     {
         // blocked W[col][part][key][64]: part 0,1 = aL halves, 2,3 = Y halves
@@ -332,7 +399,7 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
         if (!encode(&P.tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Wc, cdims, cstrides, cbox, CU_TENSOR_MAP_SWIZZLE_NONE))
             return TC_FAIL("tensor map / argument check");
-        if (g.T > 1 || wide) {
+        if (stats || wide) {
             cuuint32_t box128[4] = {64, (cuuint32_t)kAKC, 1, 1};
             if (!encode(&P.tw128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box128,
                         CU_TENSOR_MAP_SWIZZLE_128B))
@@ -344,6 +411,7 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
         }
         if (g.T > 1) {
             // hat_alpha_R[bh*gq][key][j][128] bf16
+            __nv_bfloat16* AR = reinterpret_cast<__nv_bfloat16*>(wsb + lay.ar);
             cuuint64_t adims[4] = {128, (cuuint64_t)g.s2, (cuuint64_t)g.nkeys, (cuuint64_t)g.bh * g.gq};
             cuuint64_t astr[3] = {256, (cuuint64_t)g.s2 * 256, (cuuint64_t)g.s2 * 256 * g.nkeys};
             cuuint32_t abox_st[4] = {64, 1, 32, 1};
@@ -355,48 +423,118 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
                 return TC_FAIL("tensor map / argument check");
         }
     }
-
-    cudaError_t e;
-    const int smem_row = RowSmem::kTotal + 1024;
-    const int smem_col = ColSmem::kTotal + 1024;
-    if ((e = cudaFuncSetAttribute(tc_row_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_row)) != cudaSuccess)
-        return e;
-    if ((e = cudaFuncSetAttribute(tc_column_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_col)) !=
-        cudaSuccess)
-        return e;
-
-    const int sms = num_sms();
-    const int smem_alpha = AlphaSmem::kTotal + 1024;
-    const int smem_wide = WideSmem::kTotal + 1024;
-    if (wide && (e = cudaFuncSetAttribute(tc_column_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_wide)) !=
-                    cudaSuccess)
-        return e;
+    (void)rows;
+    const int sms = num_sms(dev);
+    T->g = g;
+    T->wide = wide;
+    T->smem_row = RowSmem::kTotal + 1024;
+    T->smem_col = ColSmem::kTotal + 1024;
+    T->smem_alpha = AlphaSmem::kTotal + 1024;
+    T->smem_wide = WideSmem::kTotal + 1024;
+    T->smem_pair = RowPSmem::kTotal + 1024;
     const int64_t witems = ncols * ((g.s1 + 127) / 128);
-    const int grid_wide = witems < sms ? (int)witems : sms;
-    if (g.T > 1 &&
-        (e = cudaFuncSetAttribute(tc_alpha_r_stage, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_alpha)) !=
-            cudaSuccess)
-        return e;
+    T->grid_wide = witems < sms ? (int)witems : sms;
     const int64_t key_rows = (int64_t)g.bh * g.s1 * row_groups(g) * g.gk;   // row-stage key rows
-    const int grid_row = key_rows < sms ? (int)key_rows : sms;
+    T->grid_row = key_rows < sms ? (int)key_rows : sms;
     // half-packed row stage (two M=64 (query tile, row) halves per 128-lane task).  MBX_PAIR=0
     // selects the classic stage (whole query tiles per M=128 task), MBX_PAIR=1 the packed one.  Packing pays when whole
     // query tiles leave M=128 lanes idle (odd G_q); for G_q > 1 a K/V row then serves halves
     // of two items, so it is re-read once more -- cheap only while K and V sit in L2.
-    const char* pair_env = getenv("MBX_PAIR");
     const size_t kv_bytes = (size_t)g.bh * g.gk * g.s1 * g.s2 * (size_t)(g.d + g.dv) * 2;
-    const bool pair = pair_env ? pair_env[0] == '1'
-                               : g.gq == 1 || (g.gq % 2 == 1 && kv_bytes <= ((size_t)48 << 20));
-    const int smem_pair = RowPSmem::kTotal + 1024;
-    if (pair && (e = cudaFuncSetAttribute(tc_row_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_pair)) !=
-                    cudaSuccess)
-        return e;
+    T->pair = o.pair >= 0 ? o.pair == 1 : g.gq == 1 || (g.gq % 2 == 1 && kv_bytes <= ((size_t)48 << 20));
     const int64_t pair_tasks = (int64_t)g.bh * ((g.gq * g.s1 + 1) / 2) * g.gk;
-    const int grid_pair = pair_tasks < sms ? (int)pair_tasks : sms;
+    T->grid_pair = pair_tasks < sms ? (int)pair_tasks : sms;
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
-    const int grid_col = ngroups < sms ? (int)ngroups : sms;
+    T->grid_col = ngroups < sms ? (int)ngroups : sms;
     const int64_t aitems = ncols * ((g.nkeys + kAKC - 1) / kAKC);
-    const int grid_alpha = aitems < sms ? (int)aitems : sms;
+    T->grid_alpha = aitems < sms ? (int)aitems : sms;
+    return cudaSuccess;
+}
+
+// Launch-parameter cache: keyed by the geometry, pointers, device and option version.
+struct PlanKey {
+    Geometry g;
+    const void *q, *k, *v, *out, *ws;
+    float *lf, *rf;
+    int dev;
+    unsigned opt_version;
+};
+static bool key_eq(const PlanKey& a, const PlanKey& b) { return memcmp(&a, &b, sizeof(PlanKey)) == 0; }
+
+struct PlanCache {
+    static constexpr int kSlots = 16;
+    PlanKey key[kSlots];
+    TcPlan plan[kSlots];
+    unsigned long long used[kSlots] = {};
+    unsigned long long tick = 0;
+    int n = 0;
+};
+static PlanCache g_plans;
+static std::mutex g_plans_mu;
+
+static cudaError_t get_plan(const Geometry& g, const void* q, const void* k, const void* v, void* out,
+                            float* lf, float* rf, void* ws, int dev, TcPlan* out_plan) {
+    PlanKey key;
+    memset(&key, 0, sizeof(key));   // padding bytes take part in the comparison
+    key.g = g;
+    key.q = q; key.k = k; key.v = v; key.out = out; key.ws = ws;
+    key.lf = lf; key.rf = rf;
+    key.dev = dev;
+    key.opt_version = options().version;
+    {
+        std::lock_guard<std::mutex> lock(g_plans_mu);
+        for (int i = 0; i < g_plans.n; ++i)
+            if (key_eq(g_plans.key[i], key)) {
+                g_plans.used[i] = ++g_plans.tick;
+                *out_plan = g_plans.plan[i];
+                return cudaSuccess;
+            }
+    }
+    TcPlan p;
+    cudaError_t e = build_plan(g, q, k, v, out, lf, rf, ws, dev, &p);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_plans_mu);
+    int slot = g_plans.n < PlanCache::kSlots ? g_plans.n++ : 0;
+    if (g_plans.n == PlanCache::kSlots)
+        for (int i = 1; i < PlanCache::kSlots; ++i)
+            if (g_plans.used[i] < g_plans.used[slot]) slot = i;
+    g_plans.key[slot] = key;
+    g_plans.plan[slot] = p;
+    g_plans.used[slot] = ++g_plans.tick;
+    *out_plan = p;
+    return cudaSuccess;
+}
+
+// Dynamic shared-memory limits: set once per device (not per call).
+static cudaError_t ensure_attributes(int dev) {
+    static bool done[64] = {};
+    static std::mutex mu;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[dev]) return cudaSuccess;
+    cudaError_t e;
+    const struct { const void* fn; int smem; } k[] = {
+        {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage, ColSmem::kTotal + 1024},
+        {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
+        {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}};
+    for (auto& x : k)
+        if ((e = cudaFuncSetAttribute(x.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x.smem)) != cudaSuccess)
+            return e;
+    done[dev] = true;
+    return cudaSuccess;
+}
+
+static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
+                                  float* l_factor, float* r_factor, void* workspace, int dev, cudaStream_t stream) {
+    cudaError_t e = ensure_attributes(dev);
+    if (e != cudaSuccess) return e;
+    TcPlan T;
+    if ((e = get_plan(g0, q, k, v, out, l_factor, r_factor, workspace, dev, &T)) != cudaSuccess) return e;
+    const Geometry& g = T.g;
+    TcParams& P = T.P;
+    const bool pdl = options().pdl != 0;
+    const bool verbose = options().verbose != 0;
+    const bool factors = l_factor || r_factor;
     // Every launch after the first uses programmatic dependent launch: its CTAs set up
     // while the previous stage drains and wait (griddepcontrol.wait) before touching
     // the workspace.  The first launch is ordinary, so it never overlaps the previous
@@ -412,42 +550,49 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = (nlaunch++ > 0 && pdl_enabled()) ? 1 : 0;
+        cfg.numAttrs = (nlaunch++ > 0 && pdl) ? 1 : 0;
         cudaError_t le = cudaLaunchKernelExC(&cfg, fn, args);
-        if (le != cudaSuccess && getenv("MBX_VERBOSE"))
+        if (le != cudaSuccess && verbose)
             fprintf(stderr, "mbx tc_forward: launch %d (grid %d, smem %d) failed: %s\n", nlaunch, grid, smem,
                     cudaGetErrorString(le));
         return le;
     };
+    auto column = [&](int mode) -> cudaError_t {
+        if (T.wide) {
+            ProfScope p("tc_column_wide", stream);
+            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+            return launch((const void*)tc_column_wide, T.grid_wide, kWideThreads, T.smem_wide, args);
+        }
+        ProfScope p("tc_column_stage", stream);
+        void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+        return launch((const void*)tc_column_stage, T.grid_col, kColThreads, T.smem_col, args);
+    };
+    auto alpha = [&](int amode) -> cudaError_t {
+        ProfScope p(amode ? "tc_alpha_l_export" : "tc_alpha_r_stage", stream);
+        void* args[] = {(void*)&P, (void*)&g, (void*)&amode};
+        return launch((const void*)tc_alpha_r_stage, T.grid_alpha, kAlphaThreads, T.smem_alpha, args);
+    };
     // refinements (solver.py:184-195): row stage (A = Q at t = 0, hat_alpha_R after), then either
-    // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1)
+    // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1).  With factor
+    // export the last refinement also runs the statistics pass and writes L' from it
+    // (factors.py:57-79 layout); R' comes from the last row stage's softmax.
     for (int t = 0; t < g.T; ++t) {
-        int last = t == g.T - 1, amode = t > 0, mode = last ? 0 : 1;
-        if (pair) {
+        int last = t == g.T - 1, amode = t > 0;
+        if (T.pair) {
             ProfScope p("tc_row_pair", stream);
             void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
-            if ((e = launch((const void*)tc_row_pair, grid_pair, 448, smem_pair, args)) != cudaSuccess) return e;
+            if ((e = launch((const void*)tc_row_pair, T.grid_pair, 448, T.smem_pair, args)) != cudaSuccess) return e;
         } else {
             ProfScope p("tc_row_stage", stream);
             void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
-            if ((e = launch((const void*)tc_row_stage, grid_row, kRowThreads, smem_row, args)) != cudaSuccess) return e;
-        }
-        if (wide) {
-            ProfScope p("tc_column_wide", stream);
-            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
-            if ((e = launch((const void*)tc_column_wide, grid_wide, kWideThreads, smem_wide, args)) != cudaSuccess)
-                return e;
-        } else {
-            ProfScope p("tc_column_stage", stream);
-            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
-            if ((e = launch((const void*)tc_column_stage, grid_col, kColThreads, smem_col, args)) != cudaSuccess)
+            if ((e = launch((const void*)tc_row_stage, T.grid_row, kRowThreads, T.smem_row, args)) != cudaSuccess)
                 return e;
         }
         if (!last) {
-            ProfScope p("tc_alpha_r_stage", stream);
-            void* args[] = {(void*)&P, (void*)&g};
-            if ((e = launch((const void*)tc_alpha_r_stage, grid_alpha, kAlphaThreads, smem_alpha, args)) != cudaSuccess)
-                return e;
+            if ((e = column(1)) != cudaSuccess || (e = alpha(0)) != cudaSuccess) return e;
+        } else {
+            if (factors && l_factor && ((e = column(1)) != cudaSuccess || (e = alpha(1)) != cudaSuccess)) return e;
+            if ((e = column(0)) != cudaSuccess) return e;
         }
     }
     return cudaGetLastError();
@@ -458,12 +603,16 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
 // half's launches fill the ramp-up and drain of the first's persistent grids (KV21: 303 ->
 // 279 us with CUDA graphs, scripts/exp_streams.py), while short problems lose to the
 // halved work per CTA (C2: 59 -> 68 us), hence the size threshold.  Halves are of the heads
-// for one batch, of the batch otherwise (even counts only).  MBX_SPLIT=0/1 overrides.
-static bool tc_split(const Geometry& g) {
+// for one batch, of the batch otherwise (even counts only).  MBX_FLAG_SPLIT / NO_SPLIT (or
+// the MBX_SPLIT option) override the threshold.
+static bool tc_split(const Geometry& g, int flags) {
     const int B = g.bh / g.heads;
     if (B == 1 ? g.heads % 2 != 0 : B % 2 != 0) return false;   // halves of the heads (B = 1) or of the batch
-    const char* e = getenv("MBX_SPLIT");
-    if (e) return e[0] == '1';
+    if (flags & MBX_FLAG_FACTORS) return false;
+    if (flags & MBX_FLAG_NO_SPLIT) return false;
+    if (flags & MBX_FLAG_SPLIT) return true;
+    const int o = options().split;
+    if (o >= 0) return o == 1;
     return (size_t)g.bh * g.gq * g.s2 * g.nkeys >= ((size_t)600 << 10);   // workspace rows
 }
 static Geometry half_heads(const Geometry& g) {   // B = 1: first half of the heads; else of the batch
@@ -473,46 +622,82 @@ static Geometry half_heads(const Geometry& g) {   // B = 1: first half of the he
     return h;
 }
 
-struct SideStream {
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-static std::mutex g_side_mu;
-
-size_t tc_workspace_bytes(const Geometry& g) {
-    if (tc_split(g)) return 2 * align256(tc_workspace_one(half_heads(g)));
-    return tc_workspace_one(g);
+size_t tc_workspace_bytes(const Geometry& g, int flags) {
+    if (tc_split(g, flags)) return 2 * align256(tc_layout(half_heads(g)).total);
+    return tc_layout(g).total;
 }
 
-cudaError_t tc_forward(const Geometry& g, const void* q, const void* k, const void* v, void* out, void* workspace,
-                       cudaStream_t stream) {
-    if (!tc_split(g)) return tc_forward_one(g, q, k, v, out, workspace, stream);
+// Side stream + fork/join events of one (device, caller stream); created all-or-nothing.
+struct SideStream {
+    int dev;
+    cudaStream_t caller;
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+};
+static std::mutex g_side_mu;
+static SideStream* g_sides = nullptr;
+static int g_nsides = 0, g_cap_sides = 0;
+
+static SideStream* side_for(int dev, cudaStream_t caller, bool may_create) {
+    std::lock_guard<std::mutex> lock(g_side_mu);
+    for (int i = 0; i < g_nsides; ++i)
+        if (g_sides[i].dev == dev && g_sides[i].caller == caller) return &g_sides[i];
+    if (!may_create) return nullptr;
+    SideStream s{dev, caller, nullptr, nullptr, nullptr};
+    int prio = 0;
+    cudaStreamGetPriority(caller, &prio);   // the side stream inherits the caller's priority
+    if (cudaStreamCreateWithPriority(&s.side, cudaStreamNonBlocking, prio) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamDestroy(s.side);
+        return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventDestroy(s.fork);
+        cudaStreamDestroy(s.side);
+        return nullptr;
+    }
+    if (g_nsides == g_cap_sides) {   // entries are never freed: pointers stay valid
+        const int cap = g_cap_sides ? 2 * g_cap_sides : 8;
+        SideStream* grown = new SideStream[cap];
+        for (int i = 0; i < g_nsides; ++i) grown[i] = g_sides[i];
+        // old array intentionally leaked: callers may hold pointers into it
+        g_sides = grown;
+        g_cap_sides = cap;
+    }
+    g_sides[g_nsides] = s;
+    return &g_sides[g_nsides++];
+}
+
+cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* k, const void* v, void* out,
+                       float* l_factor, float* r_factor, void* workspace, cudaStream_t stream) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const bool factors = l_factor || r_factor;
+    SideStream* ss = nullptr;
+    if (!factors && tc_split(g, flags)) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if ((e = cudaStreamIsCapturing(stream, &cs)) != cudaSuccess) return e;
+        // never create streams/events inside a capture: split only if this caller's side exists
+        ss = side_for(dev, stream, cs == cudaStreamCaptureStatusNone);
+    }
+    if (!ss) {
+        Geometry g1 = g;
+        return tc_forward_one(g1, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
+    }
     const Geometry h = half_heads(g);
-    const size_t wsh = align256(tc_workspace_one(h));
+    const size_t wsh = align256(tc_layout(h).total);
     auto at = [&](const void* p, const int64_t* st) {   // start of the second half (bf16 elements)
         const size_t off = g.bh == g.heads ? (size_t)h.heads * (size_t)st[1] : (size_t)(h.bh / h.heads) * (size_t)st[0];
         return reinterpret_cast<const char*>(p) + off * 2;
     };
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    static SideStream sides[64];
-    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-    // one enqueue at a time per process: the fork / join events are shared
-    std::lock_guard<std::mutex> lock(g_side_mu);
-    SideStream& ss = sides[dev];
-    if (!ss.side) {
-        if ((e = cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming)) != cudaSuccess ||
-            (e = cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming)) != cudaSuccess)
-            return e;
-    }
-    if ((e = cudaEventRecord(ss.fork, stream)) != cudaSuccess || (e = cudaStreamWaitEvent(ss.side, ss.fork, 0)) != cudaSuccess)
+    if ((e = cudaEventRecord(ss->fork, stream)) != cudaSuccess || (e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess)
         return e;
-    cudaError_t e1 = tc_forward_one(h, q, k, v, out, workspace, stream);
+    cudaError_t e1 = tc_forward_one(h, q, k, v, out, nullptr, nullptr, workspace, dev, stream);
     cudaError_t e2 = tc_forward_one(h, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
-                                    reinterpret_cast<char*>(workspace) + wsh, ss.side);
-    if ((e = cudaEventRecord(ss.join, ss.side)) != cudaSuccess || (e = cudaStreamWaitEvent(stream, ss.join, 0)) != cudaSuccess)
+                                    nullptr, nullptr, reinterpret_cast<char*>(workspace) + wsh, dev, ss->side);
+    // the join is recorded even if a half failed, so the side stream never dangles outside a capture
+    if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess || (e = cudaStreamWaitEvent(stream, ss->join, 0)) != cudaSuccess)
         return e;
     return e1 != cudaSuccess ? e1 : e2;
 }

@@ -11,6 +11,10 @@
 //   MMA2  alpha_R[key, :] = P^T . Q_col                  128 x 128 x s1p
 //   epilogue: / max(c_R, eps) -> bf16 -> staging -> TMA store into
 //   hat_alpha_R[bh][a][key][j][128] (the next row stage's A rows).
+// mode 1 (factor export after the last refinement's statistics pass): only the
+// normalised P^T = L is needed; each thread writes its key's L[l] for every query
+// row l straight into L' (c1_q, c2, c1_kv, c2, s2, s1, s1) (factors.py:57-79) and
+// MMA2 / the alpha_R epilogue are skipped.
 constexpr int kAlphaThreads = 192;   // producer, MMA, 4 x softmax / epilogue
 constexpr int kAKC = 128;            // keys per item
 struct AlphaSmem {
@@ -27,7 +31,8 @@ struct AlphaSmem {
 static_assert(AlphaSmem::kTotal + 1024 <= 232448, "alpha_R stage exceeds 227 KB of shared memory");
 
 __global__ void __launch_bounds__(kAlphaThreads, 1)
-tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
+tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
+    const bool lexp = mode == 1;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AlphaSmem::kBars);
@@ -127,7 +132,10 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             // which the softmax threads finish before arriving on p_full(it))
             mbar_wait(&p_full[b], (it >> 1) & 1);
             tc_fence_after();
-            if (leader) {
+            if (leader && lexp) {   // L export: no alpha_R product
+                mma_commit(&o_full[b]);
+                mma_commit(&ld_empty[b]);
+            } else if (leader) {
                 for (int kk = 0; kk < s1p / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
                     mma_bf16(tmem + 256 + b * 128,
                              desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
@@ -158,6 +166,13 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             const float cl = reinterpret_cast<const float*>(base + AlphaSmem::kC)[r] * kLog2e;
             float cr = 0.f;
             const uint32_t prow = smem_u32(base + AlphaSmem::kP) + r * 128;
+            // L' row of this key: [bh][a][c][j][l][k] with key = c s1 + k
+            float* lrow = nullptr;
+            if (lexp && key_ok) {
+                const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
+                const int c = key / g.s1, kk = key - c * g.s1;
+                lrow = P.lfac + ((((int64_t)(bh * g.gq + a) * g.gk + c) * g.s2 + j) * g.s1) * g.s1 + kk;
+            }
             for (int l0 = 0; l0 < s1p; l0 += 32) {   // 32 query rows l per pass
                 float x[32];
                 tmem_ld32(tmem + b * 128 + lane_off + l0, x);
@@ -168,6 +183,14 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
                     const float e = ex2(fmaf(x[i], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
                     p[i] = (l < g.s1 && key_ok) ? e : 0.f;
                     cr += p[i];
+                }
+                if (lexp) {
+                    if (lrow) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (l0 + i < g.s1) lrow[(int64_t)(l0 + i) * g.s1] = p[i];
+                    }
+                    continue;
                 }
                 // P^T row (keys on rows, l along K): 64-l chunk l0 / 64, logical 16 B chunks (l0 % 64) / 8 ..
                 const uint32_t pr = prow + (l0 >> 6) * 16384;
@@ -182,6 +205,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g) {
             fence_proxy_async_smem();
             tc_fence_before();
             mbar_arrive(&p_full[b]);
+            if (lexp) continue;
             // epilogue of this item: hat_alpha_R[key, :] = D2[key, :] / max(c_R, eps)
             mbar_wait(&o_full[b], (it >> 1) & 1);
             tc_fence_after();

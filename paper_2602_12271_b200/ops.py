@@ -78,6 +78,8 @@ def prepare(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor
         raise SolverError("q, k, v must be (B, H, N, d)")
     if q.dtype not in _DTYPES or k.dtype != q.dtype or v.dtype != q.dtype or out.dtype != q.dtype:
         raise SolverError(f"q, k, v, out must share dtype float32 or bfloat16, got {q.dtype}")
+    if not (k.device == q.device and v.device == q.device and out.device == q.device):
+        raise SolverError("q, k, v and out must live on one device")
     B, H, nq, d = q.shape
     if k.shape[:2] != (B, H) or v.shape[:2] != (B, H):
         raise SolverError("q, k, v batch/head dims differ")
@@ -119,15 +121,59 @@ def _raise_mapped(err: _lib.MbxError):
     raise err
 
 
+# Prepared descriptors keyed by everything they encode (shapes, strides, dtype, device,
+# plan, solver settings, flags).  The descriptor holds no data pointers, so one entry
+# serves every call with the same geometry; the lowered plan is kept alive by the entry.
+_PREP: dict = {}
+# Workspaces per (device, stream): uses on one stream are ordered by that stream.
+_WS: dict = {}
+
+
+def _prepared(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags):
+    key = (q.shape, q.stride(), k.shape, k.stride(), v.shape, v.stride(), out.shape, out.stride(),
+           q.dtype, q.device, id(low), iterations, scale, eps_div, eps_log, flags)
+    hit = _PREP.get(key)
+    if hit is not None and hit[0] is low:
+        return hit[1], hit[2]
+    prep = prepare(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags)
+    lib = _lib.load()
+    try:
+        _lib.check(lib.mbx_validate(ctypes.byref(prep.desc)))
+    except _lib.MbxError as e:
+        _raise_mapped(e)
+    nbytes = lib.mbx_workspace_bytes(ctypes.byref(prep.desc))
+    if len(_PREP) > 512:
+        _PREP.clear()
+    _PREP[key] = (low, prep, nbytes)
+    return prep, nbytes
+
+
+def _workspace(device: torch.device, stream, nbytes: int) -> torch.Tensor:
+    key = (device.index, stream)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
 def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_log=1e-300,
-            out=None, return_factors=False, force_generic=False, workspace=None):
+            out=None, return_factors=False, force_generic=False, workspace=None, split=None):
     """Run ``mbx_forward``; returns out or (out, L', R') with fp32 factors of
-    shape (B, H, c1_q, c2, c1_kv, c2, s2, s1, s1) / (..., s1, s2, s2)."""
+    shape (B, H, c1_q, c2, c1_kv, c2, s2, s1, s1) / (..., s1, s2, s2).
+
+    ``split``: None = the library's choice of concurrent head halves, True / False
+    force it on / off.  The call is enqueued on the current stream of q's device
+    (that device is made current for the call)."""
     lib = _lib.load()
     if out is None:
         out = torch.empty(q.shape[:3] + (v.shape[3],), dtype=q.dtype, device=q.device)
     flags = _lib.FLAG_FORCE_GENERIC if force_generic else 0
-    prep = prepare(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags)
+    if return_factors:
+        flags |= _lib.FLAG_FACTORS
+    if split is not None:
+        flags |= _lib.FLAG_SPLIT if split else _lib.FLAG_NO_SPLIT
+    prep, nbytes = _prepared(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags)
     lf = rf = None
     if return_factors:
         B, H = q.shape[:2]
@@ -135,25 +181,19 @@ def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_
                          dtype=torch.float32, device=q.device)
         rf = torch.empty((B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s1, low.s2, low.s2),
                          dtype=torch.float32, device=q.device)
-    try:
-        _lib.check(lib.mbx_validate(ctypes.byref(prep.desc)))
-    except _lib.MbxError as e:
-        _raise_mapped(e)
-    nbytes = lib.mbx_workspace_bytes(ctypes.byref(prep.desc))
-    if return_factors:   # factor export runs on the SIMT path; size its workspace
-        prep.desc.flags |= _lib.FLAG_FORCE_GENERIC
-        nbytes = lib.mbx_workspace_bytes(ctypes.byref(prep.desc))
-    if workspace is None or workspace.numel() < nbytes:
-        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device)
-    stream = torch.cuda.current_stream(q.device).cuda_stream
-    st = lib.mbx_forward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                         out.data_ptr(), lf.data_ptr() if lf is not None else None,
-                         rf.data_ptr() if rf is not None else None,
-                         workspace.data_ptr(), nbytes, stream)
-    try:
-        _lib.check(st)
-    except _lib.MbxError as e:
-        _raise_mapped(e)
+    with torch.cuda.device(q.device):
+        stream = torch.cuda.current_stream(q.device).cuda_stream
+        if workspace is None or workspace.numel() < nbytes:
+            workspace = _workspace(q.device, stream, nbytes)
+        st = lib.mbx_forward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                             out.data_ptr(), lf.data_ptr() if lf is not None else None,
+                             rf.data_ptr() if rf is not None else None,
+                             workspace.data_ptr(), nbytes, stream)
+    if st != 0:
+        try:
+            _lib.check(st)
+        except _lib.MbxError as e:
+            _raise_mapped(e)
     if return_factors:
         return out, lf, rf
     return out
@@ -169,9 +209,10 @@ def apply(l_factor: torch.Tensor, r_factor: torch.Tensor, v: torch.Tensor, low: 
     prep = prepare(q_like, v, v, out, low)
     nbytes = lib.mbx_apply_workspace_bytes(ctypes.byref(prep.desc))
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=v.device)
-    st = lib.mbx_apply(ctypes.byref(prep.desc), l_factor.contiguous().data_ptr(),
-                       r_factor.contiguous().data_ptr(), v.data_ptr(), out.data_ptr(),
-                       ws.data_ptr(), nbytes, torch.cuda.current_stream(v.device).cuda_stream)
+    with torch.cuda.device(v.device):
+        st = lib.mbx_apply(ctypes.byref(prep.desc), l_factor.contiguous().data_ptr(),
+                           r_factor.contiguous().data_ptr(), v.data_ptr(), out.data_ptr(),
+                           ws.data_ptr(), nbytes, torch.cuda.current_stream(v.device).cuda_stream)
     try:
         _lib.check(st)
     except _lib.MbxError as e:
@@ -179,11 +220,52 @@ def apply(l_factor: torch.Tensor, r_factor: torch.Tensor, v: torch.Tensor, low: 
     return out
 
 
-def selected_path(q, k, v, low: Lowered, iterations=1) -> str:
+def selected_path(q, k, v, low: Lowered, iterations=1, return_factors=False) -> str:
     lib = _lib.load()
     out = torch.empty(q.shape[:3] + (v.shape[3],), dtype=q.dtype, device=q.device)
-    prep = prepare(q, k, v, out, low, iterations)
+    prep = prepare(q, k, v, out, low, iterations, flags=_lib.FLAG_FACTORS if return_factors else 0)
     return {0: "simt", 1: "tcgen05"}.get(lib.mbx_selected_path(ctypes.byref(prep.desc)), "invalid")
+
+
+def lower_for(plan, q_tokens: int, kv_tokens: int, kv_frames: int | None = None) -> Lowered:
+    """The (cached) kernel lowering of ``plan`` for a square or chunked-KV problem."""
+    if kv_frames is None and q_tokens == kv_tokens:
+        return _lower_square_cached(plan)
+    if not isinstance(plan, TilePlan):
+        raise LayoutError("chunked-KV needs a TilePlan")
+    s = plan.shape
+    if kv_frames is not None and kv_frames != s.f:
+        raise LayoutError(f"kv_frames {kv_frames} != plan frames {s.f}")
+    hw = s.h * s.w
+    if q_tokens % hw:
+        raise SolverError("query tokens are not a whole number of frames")
+    return _lower_chunked_cached(plan, q_tokens // hw)
+
+
+# ---------------------------------------------------------------- torch custom op
+# ``torch.ops.monarch_b200.monarch_attention`` makes the operator visible to
+# torch.compile / FakeTensor tracing and is where autograd attaches.  The plan is
+# not a tensor: callers register its lowering under a string key (``plan_key``).
+_LOWERED: dict[str, Lowered] = {}
+
+
+def plan_key(low: Lowered) -> str:
+    key = f"{low.c1_q},{low.c1_kv},{low.c2},{low.s1},{low.s2},{low.n_q},{low.n_kv},{low.grid},{low.nbhd}," \
+          f"{'id' if low.q_order is None else hash(low.q_order.tobytes())}," \
+          f"{'id' if low.kv_order is None else hash(low.kv_order.tobytes())}"
+    _LOWERED.setdefault(key, low)
+    return key
+
+
+@torch.library.custom_op("monarch_b200::monarch_attention", mutates_args=())
+def _monarch_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: str, iterations: int,
+                scale: float) -> torch.Tensor:
+    return forward(q, k, v, _LOWERED[plan], iterations, scale)
+
+
+@_monarch_op.register_fake
+def _monarch_op_fake(q, k, v, plan, iterations, scale):
+    return q.new_empty(q.shape[:3] + (v.shape[3],))
 
 
 def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = None,
@@ -195,19 +277,16 @@ def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = 
     solver.py:114).  With ``kv_frames`` unset the problem is square; for a
     chunked-KV rollout pass the plan over the full (f_kv, h, w) key grid and
     q holding the last ``q_frames = q.shape[2] // (h*w)`` frames.
+
+    Eager calls go straight to the C ABI; under torch.compile tracing, or when
+    autograd needs a graph, the call goes through the registered custom op.
     """
-    if kv_frames is None and q.shape[2] == k.shape[2]:
-        low = _lower_square_cached(plan)
-    else:
-        if not isinstance(plan, TilePlan):
-            raise LayoutError("chunked-KV needs a TilePlan")
-        s = plan.shape
-        if kv_frames is not None and kv_frames != s.f:
-            raise LayoutError(f"kv_frames {kv_frames} != plan frames {s.f}")
-        hw = s.h * s.w
-        if q.shape[2] % hw:
-            raise SolverError("query tokens are not a whole number of frames")
-        low = _lower_chunked_cached(plan, q.shape[2] // hw)
+    low = lower_for(plan, q.shape[2], k.shape[2], kv_frames)
+    traced = torch.compiler.is_compiling()
+    needs_grad = torch.is_grad_enabled() and (q.requires_grad or k.requires_grad or v.requires_grad)
+    if (traced or needs_grad) and not (return_factors or force_generic or out is not None):
+        sc = float(scale) if scale is not None else 1.0 / math.sqrt(q.shape[3])
+        return torch.ops.monarch_b200.monarch_attention(q, k, v, plan_key(low), iterations, sc)
     return forward(q, k, v, low, iterations, scale, out=out, return_factors=return_factors,
                    force_generic=force_generic)
 
@@ -250,7 +329,9 @@ def monarch_attention_host(q, k, v, plan, iterations: int = 1, scale: float | No
     qh, kh, vh = (x.contiguous().reshape(1, bh, x.shape[2], x.shape[3]) for x in (q, k, v))
     if out is None:
         out = torch.empty(q.shape[:3] + (v.shape[3],), dtype=q.dtype, pin_memory=True)
-    oh = out.reshape(1, bh, q.shape[2], v.shape[3])
+    if out.is_cuda or not out.is_contiguous() or out.shape != q.shape[:3] + (v.shape[3],):
+        raise SolverError("out must be a contiguous host tensor of shape (B, H, N_q, d_v)")
+    oh = out.view(1, bh, q.shape[2], v.shape[3])
     n = max(1, min(bh, chunks or 2))
     comp = torch.cuda.current_stream(dev)
     s_out = _d2h_stream(dev)
@@ -279,4 +360,5 @@ def monarch_attention_host(q, k, v, plan, iterations: int = 1, scale: float | No
 
 
 __all__ = ["monarch_attention", "monarch_attention_host", "forward", "apply", "prepare", "selected_path",
+           "lower_for", "plan_key",
            "SolverError", "BlockConfig", "TilePlan"]

@@ -20,6 +20,21 @@ FP32_TOL = 1e-4
 BF16_TOL = 2e-2
 
 
+@pytest.fixture
+def mbx_option():
+    """Set process-wide library options (mbx_set_option) for one test, restoring them after."""
+    from paper_2602_12271_b200 import _lib
+
+    saved = []
+
+    def set_(name, val):
+        saved.append((name, _lib.set_option(name, int(val))))
+
+    yield set_
+    for name, prev in reversed(saved):
+        _lib.set_option(name, prev)
+
+
 def _t(x, dev, dtype=torch.float32):
     return torch.as_tensor(np.asarray(x), dtype=dtype, device=dev)
 
@@ -241,13 +256,13 @@ def test_wide_column_path(cuda, frames, q_frames, nb, H, T):
 @pytest.mark.parametrize("frames,q_frames,h,nb,T", [(3, 3, 30, None, 1), (5, 3, 30, None, 2), (2, 2, 30, None, 1),
                                                     (4, 4, 30, None, 1), (3, 3, 30, (3, 30, 52), 1),
                                                     (3, 3, 30, "raw", 2), (7, 3, 30, None, 3), (3, 3, 15, None, 2)])
-def test_row_stage_variants(cuda, monkeypatch, row_stage, frames, q_frames, h, nb, T):
+def test_row_stage_variants(cuda, mbx_option, row_stage, frames, q_frames, h, nb, T):
     """Both row-stage kernels -- the classic one (whole query tiles per M=128 task)
     and the half-packed one (two M=64 (query tile, row) halves per task, halves with
     the same row sharing one K/V stage) -- on G_q = 1, 2, 3, 4, a raw (117, 40) blocking
     (odd s1: a lone last half) and G_q s1 = 3 x 15 odd, against the oracle.  MBX_PAIR
-    forces the variant (read on every forward)."""
-    monkeypatch.setenv("MBX_PAIR", row_stage)
+    forces the variant."""
+    mbx_option("MBX_PAIR", row_stage)
     g = torch.Generator(device="cpu").manual_seed(frames * 13 + q_frames + 7 * T + h)
     w = 52
     shape = pk.VideoShape(frames, h, w)
@@ -303,7 +318,7 @@ def test_host_api_pipelined_matches_device(cuda, B, H, chunks, q_frames):
 
 
 @pytest.mark.parametrize("env", [{"MBX_PDL": "0"}, {"MBX_L2HINT": "0"}, {"MBX_WIDE": "1"}])
-def test_diagnostic_switches_keep_results(cuda, monkeypatch, env):
+def test_diagnostic_switches_keep_results(cuda, mbx_option, env):
     """The diagnostic switches (no programmatic dependent launch, no L2 residency
     hints, the FlashAttention-style column stage forced on s1 <= 32) change
     scheduling only: results stay within the bf16 budget of the oracle and, for
@@ -313,7 +328,7 @@ def test_diagnostic_switches_keep_results(cuda, monkeypatch, env):
     low = pk.lower_square(_sf_plan())
     ref = ops.forward(q, k, v, low, 2)
     for key, val in env.items():
-        monkeypatch.setenv(key, val)
+        mbx_option(key, val)
     out = ops.forward(q, k, v, low, 2)
     if "MBX_WIDE" in env:
         assert orc.rel_l2(out.float().cpu().numpy(), _oracle_heads(q, k, v, low, 2)) < BF16_TOL
@@ -322,8 +337,8 @@ def test_diagnostic_switches_keep_results(cuda, monkeypatch, env):
 
 
 @pytest.mark.parametrize("q_frames,T", [(3, 1), (3, 2), (1, 1)])
-def test_head_split_concurrent_halves_bitwise(cuda, monkeypatch, q_frames, T):
-    """MBX_SPLIT=1 runs the two halves of the heads concurrently on the caller's stream
+def test_head_split_concurrent_halves_bitwise(cuda, q_frames, T):
+    """split=True runs the two halves of the heads concurrently on the caller's stream
     and a side stream (the default for long problems); the result is bitwise the
     single-sequence one, square and chunked-KV."""
     g = torch.Generator(device="cpu").manual_seed(23 + T + q_frames)
@@ -332,41 +347,63 @@ def test_head_split_concurrent_halves_bitwise(cuda, monkeypatch, q_frames, T):
     k, v = (torch.randn(1, 4, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(2))
     plan = _sf_plan(frames, h, w)
     low = pk.lower_chunked(plan, q_frames)
-    monkeypatch.setenv("MBX_SPLIT", "0")
-    ref = ops.forward(q, k, v, low, T)
-    monkeypatch.setenv("MBX_SPLIT", "1")
-    out = ops.forward(q, k, v, low, T)
+    ref = ops.forward(q, k, v, low, T, split=False)
+    out = ops.forward(q, k, v, low, T, split=True)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
 
 
-def test_batch_split_concurrent_halves_bitwise(cuda, monkeypatch):
+def test_batch_split_concurrent_halves_bitwise(cuda):
     """With B even the concurrent halves are halves of the batch (odd head count here)."""
     g = torch.Generator(device="cpu").manual_seed(29)
     q, k, v = (torch.randn(2, 3, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
     low = pk.lower_square(_sf_plan())
-    monkeypatch.setenv("MBX_SPLIT", "0")
-    ref = ops.forward(q, k, v, low, 1)
-    monkeypatch.setenv("MBX_SPLIT", "1")
-    out = ops.forward(q, k, v, low, 1)
+    ref = ops.forward(q, k, v, low, 1, split=False)
+    out = ops.forward(q, k, v, low, 1, split=True)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
 
 
-def test_head_split_is_graph_capturable(cuda, monkeypatch):
-    """The side-stream fork / join of the concurrent halves records into a CUDA graph."""
-    monkeypatch.setenv("MBX_SPLIT", "1")
+def test_head_split_is_graph_capturable(cuda):
+    """The side-stream fork / join of the concurrent halves records into a CUDA graph
+    (the capture stream's side stream is created by an eager call on that stream first;
+    the library never creates streams inside a capture)."""
     g = torch.Generator(device="cpu").manual_seed(31)
     q, k, v = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
     low = pk.lower_square(_sf_plan())
     out = torch.empty_like(q)
-    ops.forward(q, k, v, low, 1, out=out)
+    ref = ops.forward(q, k, v, low, 1, split=False)
+    cap = torch.cuda.Stream()
+    cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(cap):
+        ops.forward(q, k, v, low, 1, out=out, split=True)   # creates cap's side stream
     torch.cuda.synchronize()
-    eager = out.clone()
+    assert torch.equal(out, ref)
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        ops.forward(q, k, v, low, 1, out=out)
+    with torch.cuda.graph(graph, stream=cap):
+        ops.forward(q, k, v, low, 1, out=out, split=True)
     out.zero_()
     graph.replay()
     torch.cuda.synchronize()
-    assert torch.equal(out, eager)
+    assert torch.equal(out, ref)
+
+
+def test_split_side_streams_are_per_caller_stream(cuda):
+    """Two caller streams each get their own side stream: interleaved split forwards on
+    both streams give each stream's own result (no shared fork/join events)."""
+    g = torch.Generator(device="cpu").manual_seed(37)
+    qa, ka, va, qb, kb, vb = (torch.randn(1, 4, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(6))
+    low = pk.lower_square(_sf_plan())
+    ra = ops.forward(qa, ka, va, low, 1, split=False)
+    rb = ops.forward(qb, kb, vb, low, 1, split=False)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    oa, ob = torch.empty_like(qa), torch.empty_like(qb)
+    for s_ in (sa, sb):
+        s_.wait_stream(torch.cuda.current_stream())
+    for _ in range(4):
+        with torch.cuda.stream(sa):
+            ops.forward(qa, ka, va, low, 1, out=oa, split=True)
+        with torch.cuda.stream(sb):
+            ops.forward(qb, kb, vb, low, 1, out=ob, split=True)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ra) and torch.equal(ob, rb)
