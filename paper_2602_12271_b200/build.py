@@ -37,11 +37,16 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
     """trace=True builds libmonarch_b200_trace.so with per-CTA event timestamps
-    (MBX_TRACE; a profiling aid, never loaded unless MBX_LIB points at it)."""
+    (MBX_TRACE; a profiling aid, never loaded unless MBX_LIB points at it).
+    ``variant`` + ``defines`` build libmonarch_b200_<variant>.so with extra -D flags
+    (A/B experiments, loaded through MBX_LIB only)."""
     lib = LIB.replace(".so", "_trace.so") if trace else LIB
-    if not force and not trace and not _stale():
+    if variant:
+        lib = LIB.replace(".so", f"_{variant}.so")
+    if not force and not trace and not variant and not _stale():
         return LIB
     objs = []
     tmp = os.path.join(HERE, "_build")
@@ -52,8 +57,10 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
         flags += ["-Xptxas", "-v"]
     if trace:
         flags += ["-DMBX_TRACE"]
+    flags += [f"-D{d}" for d in defines]
+    suffix = ("_trace" if trace else "") + (f"_{variant}" if variant else "")
     for src in SOURCES:
-        obj = os.path.join(tmp, src.replace(".cu", "_trace.o" if trace else ".o"))
+        obj = os.path.join(tmp, src.replace(".cu", suffix + ".o"))
         cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", obj] + flags
         subprocess.run(cmd, check=True)
         objs.append(obj)
@@ -64,4 +71,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), None)
+    defs = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv, variant=var,
+                defines=defs))

@@ -581,7 +581,7 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
         if (T.pair) {
             ProfScope p("tc_row_pair", stream);
             void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
-            if ((e = launch((const void*)tc_row_pair, T.grid_pair, 448, T.smem_pair, args)) != cudaSuccess) return e;
+            if ((e = launch((const void*)tc_row_pair, T.grid_pair, kPairThreads, T.smem_pair, args)) != cudaSuccess) return e;
         } else {
             ProfScope p("tc_row_stage", stream);
             void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};

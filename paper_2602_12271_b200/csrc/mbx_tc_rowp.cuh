@@ -8,12 +8,20 @@
 // Halves enumerate idx = k * G_q + qt; task pair p holds idx 2p, 2p+1, and halves with the
 // same k share one K/V ring stage.  Per task:
 //   MMA1  S_h = A_h . K_{c,k_h}^T     2 x (64 x 64 x 128)  A = Q (or hat_alpha_R) rows from smem
-//   softmax over i (warps 2-5), c_L to the workspace, P (bf16) back over S
+//   softmax over i: two warpgroups (warps 2-5 even tasks, 6-9 odd tasks) so one group's
+//   TMEM load / store latency hides behind the other's arithmetic; c_L to the
+//   workspace, P (bf16) back over S
 //   MMA2  [aL | Y]_h = P_h . [K | V]_{c,k_h}   2 x 2 x (64 x 128 x 64), A = P in TMEM
-//   epilogue: warps 6-9 (aL) / 10-13 (Y), per warp two 16-row TMA stores (one per half)
+//   epilogue: warps 10-13 (aL) / 14-17 (Y), per warp two 16-row TMA stores (one per half)
 // (solver.py:187-191 R update and c_L; factors.py:123 Y = R V)
 constexpr int kPKV = 5;   // K/V ring stages (one key row each), at most
-constexpr int kPSB = 3;   // S/P buffers: MMA1 runs up to three tasks ahead of MMA2
+#ifndef MBX_PAIR_SOFT_WG
+#define MBX_PAIR_SOFT_WG 1
+#endif
+constexpr int kPairSoftWG = MBX_PAIR_SOFT_WG;        // softmax warpgroups (tasks alternate between them)
+constexpr int kPSB = kPairSoftWG == 1 ? 3 : 4;       // S/P buffers: MMA1 runs up to kPSB tasks ahead of MMA2
+constexpr int kPairEpi = 2 + 4 * kPairSoftWG;        // first epilogue warp
+constexpr int kPairThreads = 32 * (kPairEpi + 8);
 struct RowPSmem {
     static constexpr int kA = 0;                         // A slots [2] x [2 d-chunks][2 halves][64 rows][128 B]
     static constexpr int kASlot = 32768;
@@ -22,14 +30,14 @@ struct RowPSmem {
     // chunk ceil(s2 / 8) x 8 rows of 128 B (7 KB at s2 = 52: five stages; 8 KB: four),
     // then 1 KB of zeros that the last chunk's MMA reads of rows >= s2 may touch
     static constexpr int kKVRegion = 5 * 4 * 7168 + 1024;
-    static constexpr int kStage = kKV + kKVRegion;       // staging [8 warps] x [16 rows][64] bf16
+    static constexpr int kStage = kKV + kKVRegion;       // per epilogue warp: [16 rows][128 B] transpose buffer
     static constexpr int kBars = kStage + 8 * 2048;
     static constexpr int kNumBars = 4 + 2 * kPKV + 2 * kPSB + 4;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
 static_assert(RowPSmem::kTotal + 1024 <= 232448, "paired row stage exceeds 227 KB of shared memory");
-// TMEM: S/P buffers [0,64) [64,128) [128,192); O_aL [192,320); O_Y [320,448)
+// TMEM: S/P buffers [0,64) .. [192,256); O_aL [256,384); O_Y [384,512)
 constexpr uint32_t kPS = 0, kPOA = 64 * kPSB, kPOY = kPOA + 128;
 
 // Task walker: tasks (bh, p, c) in order, a contiguous range per CTA; item = (bh, p).
@@ -93,7 +101,7 @@ struct PairCursor {
     }
 };
 
-__global__ void __launch_bounds__(448, 1)
+__global__ void __launch_bounds__(kPairThreads, 1)
 tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int want_y_i) {
     const bool amode = amode_i != 0, want_y = want_y_i != 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -103,8 +111,8 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
     uint64_t* a_empty = bars + 2;                  // [2] MMA1s done with it
     uint64_t* kv_full = bars + 4;                  // [nkv]
     uint64_t* kv_empty = kv_full + kPKV;           // [nkv]
-    uint64_t* s_full = kv_empty + kPKV;            // [3]
-    uint64_t* p_full = s_full + kPSB;              // [3]
+    uint64_t* s_full = kv_empty + kPKV;            // [kPSB]
+    uint64_t* p_full = s_full + kPSB;              // [kPSB]
     uint64_t* o_full = p_full + kPSB;              // [2]
     uint64_t* o_empty = o_full + 2;                // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + RowPSmem::kTmemSlot);
@@ -121,8 +129,6 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         tma_prefetch(&P.tq);
         tma_prefetch(&P.tk);
         tma_prefetch(&P.tv);
-        tma_prefetch(&P.tws16);
-        tma_prefetch(&P.tws16r);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&a_full[i], 1);
             mbar_init(&a_empty[i], 1);
@@ -315,82 +321,85 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 }
             }
         }
-    } else if (warp < 6) {
-        // ------------------------------------------------ softmax: lane = (half h, row j)
+    } else if (warp < kPairEpi) {
+        // ------------------------------------------------ softmax: lane = (half h, row j); tasks alternate
+        const int wg = (warp - 2) >> 2;       // between the warpgroups: t % kPairSoftWG == wg
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const float sl2 = g.scale * kLog2e;
         int bsel = 0, bph = 0;   // S/P buffer + phase of task t
         for (int t = 0; cur.valid; ++t, cur.advance()) {
-            const uint32_t sbuf = tmem + kPS + bsel * 64 + lane_off;
-            // M=64 pair: lane = (half lane/16, row 16 quad + lane%16); shared-row M=128: (quad/2, 32 (quad%2) + lane)
-            const bool wide = cur.nh() == 2 && cur.nrows() == 1;
-            const int hh = wide ? quad >> 1 : lane >> 4;
-            const int j = wide ? 32 * (quad & 1) + lane : quad * 16 + (lane & 15);
-            const int kr = cur.kr(hh), qt = cur.qt(hh);
-            const bool row_ok = j < g.s2 && hh < cur.nh();
-            mbar_wait(&s_full[bsel], bph);
-            if (lane == 0) TR(warp, ti, 21);
-            tc_fence_after();
-            float z[64];
-            {
-                uint32_t zr[64];
-                tmem_ld32_nw(sbuf, zr);
-                tmem_ld32_nw(sbuf + 32, zr + 32);
-                tmem_wait_ld();
+            if (t % kPairSoftWG == wg) {
+                const uint32_t sbuf = tmem + kPS + bsel * 64 + lane_off;
+                // M=64 pair: lane = (half lane/16, row 16 quad + lane%16); shared-row M=128: (quad/2, 32 (quad%2) + lane)
+                const bool wide = cur.nh() == 2 && cur.nrows() == 1;
+                const int hh = wide ? quad >> 1 : lane >> 4;
+                const int j = wide ? 32 * (quad & 1) + lane : quad * 16 + (lane & 15);
+                const int kr = cur.kr(hh), qt = cur.qt(hh);
+                const bool row_ok = j < g.s2 && hh < cur.nh();
+                mbar_wait(&s_full[bsel], bph);
+                if (lane == 0) TR(warp, ti, 21);
+                tc_fence_after();
+                float z[64];
+                {
+                    uint32_t zr[64];
+                    tmem_ld32_nw(sbuf, zr);
+                    tmem_ld32_nw(sbuf + 32, zr + 32);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 64; ++i) z[i] = __uint_as_float(zr[i]);
-            }
-#pragma unroll
-            for (int blk = 0; blk < 4; ++blk) {   // only the 16-column blocks that reach past s2
-                if (16 * blk + 16 > g.s2) {
-#pragma unroll
-                    for (int i = 16 * blk; i < 16 * blk + 16; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+                    for (int i = 0; i < 64; ++i) z[i] = __uint_as_float(zr[i]);
                 }
-            }
-            float mq[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) mq[e] = fmaxf(z[e], z[e + 8]);
+                for (int blk = 0; blk < 4; ++blk) {   // only the 16-column blocks that reach past s2
+                    if (16 * blk + 16 > g.s2) {
 #pragma unroll
-            for (int i = 16; i < 64; i += 8)
+                        for (int i = 16 * blk; i < 16 * blk + 16; ++i) z[i] = i < g.s2 ? z[i] : -1e30f;
+                    }
+                }
+                float mq[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) mq[e] = fmaxf(mq[e], z[i + e]);
-            const float m = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
-                                  fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
-            const float mb = m * sl2;
-            float p[64];
+                for (int e = 0; e < 8; ++e) mq[e] = fmaxf(z[e], z[e + 8]);
 #pragma unroll
-            for (int i = 0; i < 64; ++i) p[i] = ex2(fmaf(z[i], sl2, -mb));
-            float lq[8], aq[8];
+                for (int i = 16; i < 64; i += 8)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                lq[e] = p[e] + p[e + 8];
-                aq[e] = fmaf(p[e + 8], z[e + 8], p[e] * z[e]);
-            }
-#pragma unroll
-            for (int i = 16; i < 64; i += 8)
+                    for (int e = 0; e < 8; ++e) mq[e] = fmaxf(mq[e], z[i + e]);
+                const float m = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                                      fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+                const float mb = m * sl2;
+                // p overwrites z once its z term is in the partial sums (register pressure: 18 warps)
+                float lq[8], aq[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    lq[e] += p[i + e];
-                    aq[e] = fmaf(p[i + e], z[i + e], aq[e]);
+                    lq[e] = 0.f;
+                    aq[e] = 0.f;
                 }
-            const float l = ((lq[0] + lq[1]) + (lq[2] + lq[3])) + ((lq[4] + lq[5]) + (lq[6] + lq[7]));
-            const float A = ((aq[0] + aq[1]) + (aq[2] + aq[3])) + ((aq[4] + aq[5]) + (aq[6] + aq[7]));
-            const float inv_l = 1.f / l;
-            const float pscale = row_ok ? inv_l : 0.f;
-            uint32_t packed[32];
 #pragma unroll
-            for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(p[i] * pscale, p[i + 1] * pscale);
-            tmem_st32(sbuf, reinterpret_cast<const float*>(packed));
-            tc_fence_before();
-            mbar_arrive(&p_full[bsel]);
-            if (lane == 0) TR(warp, ti, 22);
-            if (P.rfac && want_y && row_ok)   // final R' row [bh][a][c][k][j][:] (factors.py:57-79)
-                store_r_row(P.rfac + ((((int64_t)(cur.bh * g.gq + qt) * g.gk + cur.c) * g.s1 + kr) * g.s2 + j) * g.s2,
-                            p, inv_l, g.s2);
-            if (row_ok) {   // c_L = sum R z - lse with z = scale * S (solver.py:191)
-                const int col = (cur.bh * g.gq + qt) * g.s2 + j;
-                P.wc[(int64_t)col * ckey + cur.c * g.s1 + kr] = g.scale * (A * inv_l - m) - __logf(l);
+                for (int i = 0; i < 64; i += 8)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float pe = ex2(fmaf(z[i + e], sl2, -mb));
+                        lq[e] += pe;
+                        aq[e] = fmaf(pe, z[i + e], aq[e]);
+                        z[i + e] = pe;
+                    }
+                const float l = ((lq[0] + lq[1]) + (lq[2] + lq[3])) + ((lq[4] + lq[5]) + (lq[6] + lq[7]));
+                const float A = ((aq[0] + aq[1]) + (aq[2] + aq[3])) + ((aq[4] + aq[5]) + (aq[6] + aq[7]));
+                const float inv_l = 1.f / l;
+                const float pscale = row_ok ? inv_l : 0.f;
+                uint32_t packed[32];
+#pragma unroll
+                for (int i = 0; i < 64; i += 2) packed[i >> 1] = pack_bf16(z[i] * pscale, z[i + 1] * pscale);
+                tmem_st32(sbuf, reinterpret_cast<const float*>(packed));
+                tc_fence_before();
+                mbar_arrive(&p_full[bsel]);
+                if (lane == 0) TR(warp, ti, 22);
+                if (P.rfac && want_y && row_ok)   // final R' row [bh][a][c][k][j][:] (factors.py:57-79)
+                    store_r_row(P.rfac + ((((int64_t)(cur.bh * g.gq + qt) * g.gk + cur.c) * g.s1 + kr) * g.s2 + j) * g.s2,
+                                z, inv_l, g.s2);
+                if (row_ok) {   // c_L = sum R z - lse with z = scale * S (solver.py:191)
+                    const int col = (cur.bh * g.gq + qt) * g.s2 + j;
+                    P.wc[(int64_t)col * ckey + cur.c * g.s1 + kr] = g.scale * (A * inv_l - m) - __logf(l);
+                }
             }
             if (++bsel == kPSB) {
                 bsel = 0;
@@ -398,22 +407,19 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
             }
         }
     } else {
-        // ------------------------------------------------ epilogue: warps 6-9 O_aL, 10-13 O_Y
-        const int set = warp >= 10 ? 1 : 0;
+        // ------------------------------------------------ epilogue: 4 warps O_aL, 4 warps O_Y
+        // Each lane owns one row (TMEM lane) and writes its 128 contiguous bytes per part straight
+        // from registers (st.global.v4 with the L2 evict_last policy): no staging round trips.
+        const int set = warp >= kPairEpi + 4 ? 1 : 0;
         if (set == 1 && !want_y) cur.valid = false;
         // the column stage reads W right after this launch: keep it in L2 ahead of q / k / v
         const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
-        const int nr = min(16, g.s2 - quad * 16);             // M=64 pair: rows j of this warp per half
-        const int nrw = min(32, g.s2 - 32 * (quad & 1));      // shared-row M=128: rows of half quad/2
-        uint8_t* stg = smem + RowPSmem::kStage + (warp - 6) * 2048;   // 16 rows: one store at a time
+        __nv_bfloat16* W = const_cast<__nv_bfloat16*>(P.w);
         for (int t = 0; cur.valid; ++t, cur.advance()) {
-            const int nh = cur.nh();
-            const bool wide = nh == 2 && cur.nrows() == 1;
-            const bool store_ok = wide ? nrw > 0 : nr > 0;
-            const int col0 = (cur.bh * g.gq) * g.s2 + quad * 16;   // + qt_h * s2 per half
+            const bool wide = cur.nh() == 2 && cur.nrows() == 1;
             mbar_wait(&o_full[set], t & 1);
             if (lane == 0) TR(warp, ti, 31);
             tc_fence_after();
@@ -422,60 +428,67 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
 #pragma unroll
                 for (int i = 0; i < 32; ++i) pk[0][i] = pk[1][i] = 0u;
             } else {
+                uint32_t o[2][32];
+                tmem_ld32_nw(obuf, o[0]);
+                tmem_ld32_nw(obuf + 32, o[1]);
+                tmem_wait_ld();
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    uint32_t o[32];
-                    tmem_ld32_nw(obuf + q4 * 32, o);
-                    tmem_wait_ld();
+                for (int q2 = 0; q2 < 2; ++q2)
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
-                        pk[q4 >> 1][(q4 & 1) * 16 + i] =
-                            pack_bf16(__uint_as_float(o[2 * i]), __uint_as_float(o[2 * i + 1]));
-                }
+                        pk[0][q2 * 16 + i] = pack_bf16(__uint_as_float(o[q2][2 * i]), __uint_as_float(o[q2][2 * i + 1]));
+                tmem_ld32_nw(obuf + 64, o[0]);
+                tmem_ld32_nw(obuf + 96, o[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int q2 = 0; q2 < 2; ++q2)
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        pk[1][q2 * 16 + i] = pack_bf16(__uint_as_float(o[q2][2 * i]), __uint_as_float(o[q2][2 * i + 1]));
             }
             tc_fence_before();
             mbar_arrive(&o_empty[set]);
             if (lane == 0) TR(warp, ti, 32);
-            if (store_ok && !(P.dbg & 1)) {   // dbg 1: timing experiment without the workspace stores
-                // per part, two 16-row stores: M=64 pair -> lanes 0-15 / 16-31 are halves 0 / 1;
-                // shared-row M=128 -> lanes 0-15 / 16-31 are rows j0 .. j0+15 / j0+16 .. of half quad/2
+            if (!(P.dbg & 1)) {   // dbg 1: timing experiment without the workspace stores
+                // 16 rows at a time through the warp's 2 KB buffer: each lane writes its row (swizzled
+                // 16-byte chunks), then every instruction stores 4 whole 128-byte rows (coalesced
+                // st.global.v4, L2 evict_last) -- no bulk-copy round trips between the groups.
+                const uint32_t stg = smem_u32(smem + RowPSmem::kStage + (warp - kPairEpi) * 2048);
+                const int nh = cur.nh();
+                const int64_t rstride = (int64_t)4 * g.nkeys * 64;   // bf16 elements between rows j, j + 1
 #pragma unroll
-                for (int part = 0; part < 2; ++part) {
+                for (int sub = 0; sub < 2; ++sub) {
+                    const int hs = wide ? quad >> 1 : sub;
+                    const int j0 = wide ? 32 * (quad & 1) + 16 * sub : quad * 16;
+                    const int nrows = hs < nh ? min(16, g.s2 - j0) : 0;
+                    if (nrows <= 0) continue;
+                    const int64_t col0 = (int64_t)(cur.bh * g.gq + cur.qt(hs)) * g.s2 + j0;
+                    const int key = cur.c * g.s1 + cur.kr(hs);
 #pragma unroll
-                    for (int sub = 0; sub < 2; ++sub) {
-                        int rows, key, col;
-                        if (wide) {
-                            const int hw = quad >> 1;
-                            rows = min(16, nrw - 16 * sub);
-                            key = cur.c * g.s1 + cur.kr(hw);
-                            col = (cur.bh * g.gq + cur.qt(hw)) * g.s2 + 32 * (quad & 1) + 16 * sub;
-                        } else {
-                            rows = sub < nh ? nr : 0;
-                            key = cur.c * g.s1 + cur.kr(sub);
-                            col = col0 + cur.qt(sub) * g.s2;
-                        }
-                        if (rows <= 0) continue;
-                        if (lane == 0) bulk_wait_read<0>();
-                        __syncwarp();
+                    for (int part = 0; part < 2; ++part) {
                         if ((lane >> 4) == sub) {
-                            const uint32_t srow = smem_u32(stg) + (lane & 15) * 128;
+                            const uint32_t srow = stg + (lane & 15) * 128;
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc)
                                 st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pk[part][4 * cc], pk[part][4 * cc + 1],
                                              pk[part][4 * cc + 2], pk[part][4 * cc + 3]);
                         }
-                        fence_proxy_async_smem();
                         __syncwarp();
-                        if (lane == 0) {
-                            tma_store_4d_hint(rows == 16 ? &P.tws16 : &P.tws16r, stg, 0, key, 2 * set + part, col,
-                                              w_policy);
-                            bulk_commit();
+                        __nv_bfloat16* base = W + ((col0 * 4 + 2 * set + part) * g.nkeys + key) * 64;
+                        const int ch = lane & 7;
+#pragma unroll
+                        for (int it = 0; it < 4; ++it) {
+                            const int r = it * 4 + (lane >> 3);
+                            if (r < nrows) {
+                                const uint4 v4 = ld_shared_v4u(stg + r * 128 + ((ch ^ (r & 7)) << 4));
+                                st_global_v4_hint(base + r * rstride + ch * 8, v4.x, v4.y, v4.z, v4.w, w_policy);
+                            }
                         }
+                        __syncwarp();
                     }
                 }
             }
         }
-        if (lane == 0) bulk_wait<0>();
     }
     tc_fence_before();
     __syncthreads();
