@@ -73,6 +73,8 @@ typedef enum mbx_dtype {
                                        the path for it (mbx_workspace_bytes / mbx_selected_path)     */
 #define MBX_FLAG_NO_SPLIT 0x8       /* never run the concurrent head/batch halves                   */
 #define MBX_FLAG_SPLIT 0x10         /* always run the concurrent halves when the shape allows        */
+#define MBX_FLAG_ALL_ITERS 0x20     /* export the factors of EVERY refinement: l_factor / r_factor hold
+                                       T slices [T][B][H][...] (the backward pass needs them)        */
 
 /*
  * One forward problem, batched over (batch, heads).  Tokens of a (b, h)
@@ -159,6 +161,19 @@ int mbx_apply(const mbx_desc* desc, const float* l_factor, const float* r_factor
 
 /* Workspace for mbx_apply (the Y = R V intermediate). */
 size_t mbx_apply_workspace_bytes(const mbx_desc* desc);
+
+/*
+ * Backward pass (the paper's finetuning backward; not in the
+ * reference package): gradients of sum(out * dout) with respect to q, k and v.
+ * l_factors / r_factors are the factors of every refinement as written by
+ * mbx_forward with MBX_FLAG_ALL_ITERS (T slices; for T = 1 the ordinary export).
+ * dq / dk / dv use the q / k / v strides of the descriptor, dout uses o_stride.
+ * fp32 arithmetic for both dtypes (bf16 tensors are read and written as bf16).
+ */
+int mbx_backward(const mbx_desc* desc, const void* q, const void* k, const void* v, const void* dout,
+                 const float* l_factors, const float* r_factors, void* dq, void* dk, void* dv,
+                 void* workspace, size_t workspace_bytes, void* stream);
+size_t mbx_backward_workspace_bytes(const mbx_desc* desc);
 
 /*
  * Per-kernel timing for benchmarks (thread-local).  While enabled, every

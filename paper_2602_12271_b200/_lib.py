@@ -20,13 +20,14 @@ FLAG_NO_OUTPUT = 0x2
 FLAG_FACTORS = 0x4
 FLAG_NO_SPLIT = 0x8
 FLAG_SPLIT = 0x10
+FLAG_ALL_ITERS = 0x20
 
 OK, BAD_SHAPE, BAD_PLAN, BAD_ITERS, BAD_EPS, BAD_DTYPE, NULL, WORKSPACE, UNSUPPORTED, CUDA = range(10)
 
 EXPORTS = ("mbx_version", "mbx_last_error", "mbx_validate", "mbx_workspace_bytes",
            "mbx_selected_path", "mbx_forward", "mbx_apply", "mbx_apply_workspace_bytes",
            "mbx_profile_enable", "mbx_profile_collect", "mbx_profile_collect_ex", "mbx_token_index",
-           "mbx_set_option")
+           "mbx_set_option", "mbx_backward", "mbx_backward_workspace_bytes")
 
 
 class MbxDesc(ctypes.Structure):
@@ -102,6 +103,11 @@ def load() -> ctypes.CDLL:
     lib.mbx_profile_collect_ex.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
                                            ctypes.POINTER(ctypes.c_char_p), ctypes.c_int]
     lib.mbx_profile_collect_ex.restype = ctypes.c_int
+    lib.mbx_backward.argtypes = [ctypes.POINTER(MbxDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t,
+                                 vp]
+    lib.mbx_backward.restype = ctypes.c_int
+    lib.mbx_backward_workspace_bytes.argtypes = [ctypes.POINTER(MbxDesc)]
+    lib.mbx_backward_workspace_bytes.restype = ctypes.c_size_t
     lib.mbx_set_option.argtypes = [ctypes.c_char_p, ctypes.c_int]
     lib.mbx_set_option.restype = ctypes.c_int
     if lib.mbx_version() != ABI_VERSION:

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmonarch_b200.so")
-SOURCES = ("mbx_api.cu", "mbx_generic.cu", "mbx_tc.cu")
+SOURCES = ("mbx_api.cu", "mbx_generic.cu", "mbx_tc.cu", "mbx_backward.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

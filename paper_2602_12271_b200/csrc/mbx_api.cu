@@ -245,8 +245,31 @@ int mbx_forward(const mbx_desc* desc, const void* q, const void* k, const void* 
             return fail(MBX_ERR_WORKSPACE, "workspace %zu < required %zu bytes", workspace_bytes, need);
         if (!want_out) ws.y = nullptr;
         e = mbx::generic_forward(g, desc->dtype, q, k, v, want_out ? out : nullptr, l_factor,
-                                 r_factor, ws, s);
+                                 r_factor, ws, s, (desc->flags & MBX_FLAG_ALL_ITERS) != 0);
     }
+    if (e != cudaSuccess) return fail(MBX_ERR_CUDA, "CUDA error: %s", cudaGetErrorString(e));
+    return MBX_OK;
+}
+
+size_t mbx_backward_workspace_bytes(const mbx_desc* desc) {
+    mbx::Geometry g;
+    if (validate(desc, &g) != MBX_OK) return 0;
+    return mbx::backward_workspace_bytes(g);
+}
+
+int mbx_backward(const mbx_desc* desc, const void* q, const void* k, const void* v, const void* dout,
+                 const float* l_factors, const float* r_factors, void* dq, void* dk, void* dv,
+                 void* workspace, size_t workspace_bytes, void* stream) {
+    mbx::Geometry g;
+    int st = validate(desc, &g);
+    if (st != MBX_OK) return st;
+    if (!q || !k || !v || !dout || !l_factors || !r_factors || !dq || !dk || !dv)
+        return fail(MBX_ERR_NULL, "q, k, v, dout, factors, dq, dk and dv must be non-NULL");
+    const size_t need = mbx::backward_workspace_bytes(g);
+    if (!workspace || workspace_bytes < need)
+        return fail(MBX_ERR_WORKSPACE, "workspace %zu < required %zu bytes", workspace_bytes, need);
+    cudaError_t e = mbx::backward(g, desc->dtype, q, k, v, dout, l_factors, r_factors, dq, dk, dv, workspace,
+                                  reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return fail(MBX_ERR_CUDA, "CUDA error: %s", cudaGetErrorString(e));
     return MBX_OK;
 }

@@ -1,0 +1,526 @@
+// Backward pass of the tiled MonarchAttention forward (the
+// paper's finetuning backward, PAPER.md:135-136, 644 -- not in the reference
+// package, whose SPEC.md:8 leaves it out).  fp32 SIMT kernels over the factors
+// the forward exports (R' and L' of every refinement, factors.py:57-79 layout),
+// restating the chain rule of solver.py:184-195 / factors.py:123-124:
+//
+//   forward per refinement t:  z = A_t K^T,  R = softmax_i z,  aL = R K,
+//     c_L = sum R z - lse,  S = Q aL - c_L,  L = softmax_(c,k) S,
+//     A_{t+1} = (sum_l L Q) / max(sum_l L, eps);  last: Y = R V,  O = L Y.
+//   backward (last refinement first):
+//     dL = dO . Y,  dS = L (dL - sum L dL),  dQ += dS aL,  daL = dS^T Q,  dc_L = -sum_l dS,
+//     dY = L^T dO,  dR = dY V^T + daL K^T,  dz = R (dR - sum R dR) + dc_L R (z - sum R z),
+//     dK += dz^T A_t + R^T daL,  dV += R^T dY,  dA_t = dz K;
+//     t = 0: dQ += sum_c dA_0;  t > 0: dalpha_R = dA_t / m, dc_R = -(dA_t . A_t) / m
+//     (m = max(c_R, eps), zero where clamped), dL_{t-1} = Q dalpha_R^T + dc_R, dQ += L_{t-1} dalpha_R.
+//
+// Every contraction is one launch of a strided batched GEMM (4 batch levels, a
+// two-level reduction index); the softmax backward steps are row kernels.  The
+// oracle is torch autograd of oracle/monarch_torch.py (tests/test_backward_gpu.py).
+#include "mbx_internal.h"
+
+#include <math.h>
+
+namespace mbx {
+namespace {
+
+__device__ __forceinline__ float ld(const float* p) { return *p; }
+__device__ __forceinline__ float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void store(float* p, float x) { *p = x; }
+__device__ __forceinline__ void store(__nv_bfloat16* p, float x) { *p = __float2bfloat16_rn(x); }
+
+// ---------------------------------------------------------------- batched GEMM
+// C[b][m][n] = alpha * sum_{k1 < K1, k2 < K2} A[b][m][k1][k2] B[b][k1][k2][n] (+ C if acc),
+// b = (b0, b1, b2, b3); every operand addressed by element strides (0 = broadcast).
+struct Operand {
+    const float* p;
+    int64_t s0, s1;        // A: (m, k1) / B: (n, k1) / C: (m, n)
+    int64_t s2;            // A, B: k2 stride
+    int64_t b[4];          // batch strides
+};
+struct Gemm {
+    int M, N, K1, K2;
+    int nb[4];
+    Operand A, B, C;
+    float alpha;
+    int acc;
+};
+
+constexpr int kTM = 64, kTN = 64, kTK = 16, kGemmThreads = 256;
+
+__global__ void __launch_bounds__(kGemmThreads) gemm_batched(Gemm G) {
+    __shared__ float As[kTK][kTM + 4];
+    __shared__ float Bs[kTK][kTN + 4];
+    const int tiles_n = (G.N + kTN - 1) / kTN;
+    int64_t bx = blockIdx.x;
+    const int tn = (int)(bx % tiles_n);
+    bx /= tiles_n;
+    int bi[4];
+    bi[3] = (int)(bx % G.nb[3]); bx /= G.nb[3];
+    bi[2] = (int)(bx % G.nb[2]); bx /= G.nb[2];
+    bi[1] = (int)(bx % G.nb[1]); bx /= G.nb[1];
+    bi[0] = (int)bx;
+    const int m0 = blockIdx.y * kTM, n0 = tn * kTN;
+    const float* A = G.A.p;
+    const float* B = G.B.p;
+    float* C = const_cast<float*>(G.C.p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        A += bi[i] * G.A.b[i];
+        B += bi[i] * G.B.b[i];
+        C += bi[i] * G.C.b[i];
+    }
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;   // 16 x 16 threads, 4 x 4 outputs each
+    float acc[4][4] = {};
+    const int K = G.K1 * G.K2;
+    for (int k0 = 0; k0 < K; k0 += kTK) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int idx = tid + r * kGemmThreads;   // 0 .. 1023
+            // A tile: kTK x kTM, consecutive threads walk m (A's m stride is the common small one)
+            {
+                const int kk = idx / kTM, mm = idx % kTM;
+                const int k = k0 + kk, m = m0 + mm;
+                float x = 0.f;
+                if (k < K && m < G.M) {
+                    const int k1 = k / G.K2, k2 = k - (k / G.K2) * G.K2;
+                    x = A[m * G.A.s0 + k1 * G.A.s1 + k2 * G.A.s2];
+                }
+                As[kk][mm] = x;
+            }
+            {
+                const int kk = idx / kTN, nn = idx % kTN;
+                const int k = k0 + kk, n = n0 + nn;
+                float x = 0.f;
+                if (k < K && n < G.N) {
+                    const int k1 = k / G.K2, k2 = k - (k / G.K2) * G.K2;
+                    x = B[n * G.B.s0 + k1 * G.B.s1 + k2 * G.B.s2];
+                }
+                Bs[kk][nn] = x;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < kTK; ++kk) {
+            float a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                a[i] = As[kk][ty + 16 * i];
+                b[i] = Bs[kk][tx + 16 * i];
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int m = m0 + ty + 16 * i;
+        if (m >= G.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx + 16 * j;
+            if (n >= G.N) continue;
+            float* c = C + m * G.C.s0 + n * G.C.s1;
+            const float v = G.alpha * acc[i][j];
+            *c = G.acc ? *c + v : v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- row kernels
+// dS = L (dL - D), D = sum_(c,k) L dL, in place over dL.  One warp per (bh a, j, l).
+// L, dL: [bha][c][j][l][k]
+__global__ void softmax_bwd_cols(const float* __restrict__ L, float* __restrict__ dL, int64_t rows, int gk, int s2,
+                                 int s1) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const int l = (int)(w % s1), j = (int)((w / s1) % s2);
+    const int64_t bha = w / ((int64_t)s1 * s2);
+    const int64_t cst = (int64_t)s2 * s1 * s1;
+    const int64_t base = bha * gk * cst + ((int64_t)j * s1 + l) * s1;
+    const int n = gk * s1;
+    float D = 0.f;
+    for (int x = lane; x < n; x += 32) {
+        const int64_t o = base + (x / s1) * cst + x % s1;
+        D += L[o] * dL[o];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) D += __shfl_xor_sync(0xffffffffu, D, o);
+    for (int x = lane; x < n; x += 32) {
+        const int64_t o = base + (x / s1) * cst + x % s1;
+        dL[o] = L[o] * (dL[o] - D);
+    }
+}
+
+// out[bha][c][k][j] = sign * sum_l X[bha][c][j][l][k]  (c_L / c_R reductions over the query rows)
+__global__ void sum_over_l(const float* __restrict__ X, float* __restrict__ out, int64_t n, int s2, int s1,
+                           float sign) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int j = (int)(t % s2), k = (int)((t / s2) % s1);
+    const int64_t bhac = t / ((int64_t)s2 * s1);
+    const float* x = X + (bhac * s2 + j) * s1 * s1 + k;
+    float s = 0.f;
+    for (int l = 0; l < s1; ++l) s += x[(int64_t)l * s1];
+    out[t] = sign * s;
+}
+
+// Row softmax backward of the row stage, in place over dR:
+//   dz = R (dR - sum R dR) + dcL R (z - sum R z),  one warp per row (bh,a,c,k,j) of s2 entries.
+__global__ void softmax_bwd_rows(const float* __restrict__ R, const float* __restrict__ z, float* __restrict__ dR,
+                                 const float* __restrict__ dcl, int64_t rows, int s2) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float* r = R + w * s2;
+    const float* zz = z + w * s2;
+    float* d = dR + w * s2;
+    float srd = 0.f, srz = 0.f;
+    for (int i = lane; i < s2; i += 32) {
+        srd += r[i] * d[i];
+        srz += r[i] * zz[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        srd += __shfl_xor_sync(0xffffffffu, srd, o);
+        srz += __shfl_xor_sync(0xffffffffu, srz, o);
+    }
+    const float c = dcl[w];
+    for (int i = lane; i < s2; i += 32) d[i] = r[i] * (d[i] - srd) + c * r[i] * (zz[i] - srz);
+}
+
+// A_t = alpha_R / max(c_R, eps) (rows of d features), in place.
+__global__ void normalize_rows(float* __restrict__ a, const float* __restrict__ cr, int64_t n, int d, float eps) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    a[t] /= fmaxf(cr[t / d], eps);
+}
+
+// dalpha_R = dA / m and dc_R = -(dA . A) / m (0 where c_R was clamped); in place over dA.
+__global__ void normalize_bwd(float* __restrict__ dA, const float* __restrict__ A, const float* __restrict__ cr,
+                              float* __restrict__ dcr, int64_t rows, int d, float eps) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    const float m = fmaxf(cr[w], eps);
+    float s = 0.f;
+    for (int e = lane; e < d; e += 32) {
+        s += dA[w * d + e] * A[w * d + e];
+        dA[w * d + e] /= m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) dcr[w] = cr[w] > eps ? -s / m : 0.f;
+}
+
+// dL[bha][c][j][l][k] += dcr[bha][c][k][j]  (c_R = sum_l L)
+__global__ void add_dcr(float* __restrict__ dL, const float* __restrict__ dcr, int64_t n, int s2, int s1) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int k = (int)(t % s1), j = (int)((t / ((int64_t)s1 * s1)) % s2);
+    const int64_t bhac = t / ((int64_t)s1 * s1 * s2);
+    dL[t] += dcr[(bhac * s1 + k) * s2 + j];
+}
+
+// ---------------------------------------------------------------- gathers / scatters
+__device__ __forceinline__ int64_t slot_row(const Geometry& g, const int32_t* order, int tile, int r, int j) {
+    const int l1 = tile / g.c2, j1 = tile - (tile / g.c2) * g.c2;
+    const int64_t p = ((int64_t)(l1 * g.s1 + r) * g.c2 + j1) * g.s2 + j;
+    return order ? (int64_t)order[p] : p;
+}
+
+// dst[bh][tile][r][j][e] = scale * src[b, h, row(tile, r, j), e]
+template <typename T>
+__global__ void gather_tiles(const Geometry g, const T* __restrict__ src, const int64_t* st, const int32_t* order,
+                             int tiles, int width, float scale, float* __restrict__ dst) {
+    const int64_t n = (int64_t)g.bh * tiles * g.s1 * g.s2 * width;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(t % width);
+        int64_t x = t / width;
+        const int j = (int)(x % g.s2); x /= g.s2;
+        const int r = (int)(x % g.s1); x /= g.s1;
+        const int tile = (int)(x % tiles);
+        const int bh = (int)(x / tiles);
+        const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
+        dst[t] = scale * ld(src + b * st[0] + h * st[1] + slot_row(g, order, tile, r, j) * st[2] + e);
+    }
+}
+
+template <typename T>
+__global__ void scatter_tiles(const Geometry g, const float* __restrict__ src, const int64_t* st, const int32_t* order,
+                              int tiles, int width, float scale, T* __restrict__ dst) {
+    const int64_t n = (int64_t)g.bh * tiles * g.s1 * g.s2 * width;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(t % width);
+        int64_t x = t / width;
+        const int j = (int)(x % g.s2); x /= g.s2;
+        const int r = (int)(x % g.s1); x /= g.s1;
+        const int tile = (int)(x % tiles);
+        const int bh = (int)(x / tiles);
+        const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
+        store(dst + b * st[0] + h * st[1] + slot_row(g, order, tile, r, j) * st[2] + e, scale * src[t]);
+    }
+}
+
+// ------------------------------------------------------------------ host
+struct Buf {
+    int64_t* strides;   // q, k, v, out element strides (read by the gather / scatter kernels)
+    float *Qt, *Kt, *Vt, *dOt, *dQt, *dKt, *dVt;
+    float *aL, *Y, *daL, *dY, *Ah, *dAh;
+    float *cR, *dcL, *dcR;
+    float *dL, *dLp, *z, *dR;
+};
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t layout(const Geometry& g, char* base, Buf* b) {
+    const size_t bh = g.bh, gq = g.gq, gk = g.gk, s1 = g.s1, s2 = g.s2, d = g.d, dv = g.dv;
+    const size_t tq = gq * s1 * s2, tk = gk * s1 * s2, pairs = gq * gk * s1 * s2;
+    size_t off = 0;
+    auto carve = [&](size_t floats) {
+        float* p = base ? reinterpret_cast<float*>(base + off) : nullptr;
+        off += align_up(floats * bh * sizeof(float));
+        return p;
+    };
+    Buf x{};
+    x.strides = base ? reinterpret_cast<int64_t*>(base) : nullptr;
+    off += 256;
+    x.Qt = carve(tq * d);
+    x.Kt = carve(tk * d);
+    x.Vt = carve(tk * dv);
+    x.dOt = carve(tq * dv);
+    x.dQt = carve(tq * d);
+    x.dKt = carve(tk * d);
+    x.dVt = carve(tk * dv);
+    x.aL = carve(pairs * d);
+    x.Y = carve(pairs * dv);
+    x.daL = carve(pairs * d);
+    x.dY = carve(pairs * dv);
+    if (g.T > 1) {
+        x.Ah = carve(pairs * d);
+        x.dAh = carve(pairs * d);
+        x.cR = carve(pairs);
+        x.dcR = carve(pairs);
+        x.dLp = carve(pairs * s1);
+    }
+    x.dcL = carve(pairs);
+    x.dL = carve(pairs * s1);
+    x.z = carve(pairs * s2);
+    x.dR = carve(pairs * s2);
+    if (b) *b = x;
+    return off;
+}
+
+struct Ctx {
+    const Geometry& g;
+    cudaStream_t st;
+    cudaError_t err = cudaSuccess;
+};
+
+Operand op(const float* p, int64_t s0, int64_t s1, int64_t s2, int64_t b0, int64_t b1, int64_t b2, int64_t b3) {
+    Operand o;
+    o.p = p;
+    o.s0 = s0;
+    o.s1 = s1;
+    o.s2 = s2;
+    o.b[0] = b0;
+    o.b[1] = b1;
+    o.b[2] = b2;
+    o.b[3] = b3;
+    return o;
+}
+
+void gemm(Ctx& c, const char* name, int M, int N, int K1, int K2, const int nb[4], Operand A, Operand B, Operand C,
+          float alpha, int acc) {
+    if (c.err != cudaSuccess) return;
+    Gemm G;
+    G.M = M; G.N = N; G.K1 = K1; G.K2 = K2;
+    for (int i = 0; i < 4; ++i) G.nb[i] = nb[i];
+    G.A = A; G.B = B; G.C = C;
+    G.alpha = alpha;
+    G.acc = acc;
+    const int64_t batches = (int64_t)nb[0] * nb[1] * nb[2] * nb[3];
+    dim3 grid((unsigned)(batches * ((N + kTN - 1) / kTN)), (unsigned)((M + kTM - 1) / kTM));
+    ProfScope p(name, c.st);
+    gemm_batched<<<grid, kGemmThreads, 0, c.st>>>(G);
+    c.err = cudaGetLastError();
+}
+
+unsigned blocks_for(int64_t threads, int per_block = 256) { return (unsigned)((threads + per_block - 1) / per_block); }
+
+template <typename T>
+cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, const T* dout, const float* lf,
+                       const float* rf, T* dq_out, T* dk_out, T* dv_out, char* ws, cudaStream_t stream) {
+    Buf b;
+    layout(g, ws, &b);
+    Ctx c{g, stream};
+    const int64_t bh = g.bh, gq = g.gq, gk = g.gk, s1 = g.s1, s2 = g.s2, d = g.d, dv = g.dv;
+    const int64_t bha = bh * gq;
+    const int64_t tq = gq * s1 * s2, tk = gk * s1 * s2;
+    const int64_t pairs = gq * gk * s1 * s2;            // per bh
+    const int64_t rsz = pairs * s2, lsz = pairs * s1;   // R' / L' elements per bh
+    // strides of the host q/k/v/out tensors, on the device (gather / scatter kernels read them there)
+    int64_t* dstr = b.strides;
+    {
+        int64_t h[12];
+        for (int i = 0; i < 3; ++i) {
+            h[i] = g.qs[i];
+            h[3 + i] = g.ks[i];
+            h[6 + i] = g.vs[i];
+            h[9 + i] = g.os[i];
+        }
+        cudaError_t e = cudaMemcpyAsync(dstr, h, sizeof(h), cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return e;
+    }
+    const unsigned gb = 148 * 8;
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, k, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, b.Kt);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, v, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, b.Vt);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, dout, dstr + 9, g.q_order, (int)gq, (int)dv, 1.f, b.dOt);
+    cudaMemsetAsync(b.dQt, 0, sizeof(float) * bh * tq * d, stream);
+    cudaMemsetAsync(b.dKt, 0, sizeof(float) * bh * tk * d, stream);
+    cudaMemsetAsync(b.dVt, 0, sizeof(float) * bh * tk * dv, stream);
+    if ((c.err = cudaGetLastError()) != cudaSuccess) return c.err;
+    // strides reused below (elements)
+    const int64_t qt_a = s1 * s2 * d, kt_c = s1 * s2 * d, vt_c = s1 * s2 * dv, do_a = s1 * s2 * dv;
+    const int64_t pd_a = gk * s1 * s2 * d, pd_c = s1 * s2 * d, pd_k = s2 * d;            // [a][c][k][j][d]
+    const int64_t pv_a = gk * s1 * s2 * dv, pv_c = s1 * s2 * dv, pv_k = s2 * dv;
+    const int64_t r_a = gk * s1 * s2 * s2, r_c = s1 * s2 * s2, r_k = s2 * s2;            // [a][c][k][j][i]
+    const int64_t l_a = gk * s2 * s1 * s1, l_c = s2 * s1 * s1, l_j = s1 * s1;            // [a][c][j][l][k]
+    const int64_t p_a = gk * s1 * s2, p_c = s1 * s2, p_k = s2;                            // [a][c][k][j]
+    const int nb_ack[4] = {(int)bh, (int)gq, (int)gk, (int)s1};
+    const int nb_acj[4] = {(int)bh, (int)gq, (int)gk, (int)s2};
+    const int nb_aj[4] = {(int)bh, (int)gq, 1, (int)s2};
+    const int nb_ak[4] = {(int)bh, (int)gq, 1, (int)s1};
+    const int nb_ck[4] = {(int)bh, 1, (int)gk, (int)s1};
+
+    for (int t = g.T - 1; t >= 0; --t) {
+        const float* R = rf + (size_t)t * bh * rsz;
+        const float* L = lf + (size_t)t * bh * lsz;
+        const bool last = t == g.T - 1;
+        // A_t rows: Q (t = 0) or alpha_R / max(c_R, eps) from L_{t-1} (recomputed)
+        const float* At;
+        Operand At_rows;   // as [bh][a][c][k][j][e]
+        if (t == 0) {
+            At = b.Qt;
+            At_rows = op(b.Qt, d, 0, 1, gq * qt_a, qt_a, 0, s2 * d);
+        } else {
+            const float* Lp = lf + (size_t)(t - 1) * bh * lsz;
+            // alpha_R[a][c][k][j][:] = sum_l L_{t-1}[a][c][j][l][k] Q[a][l][j][:]   (M = k, N = e, K = l)
+            gemm(c, "bwd_alpha_r", (int)s1, (int)d, 1, (int)s1, nb_acj,
+                 op(Lp, 1, 0, s1, gq * l_a, l_a, l_c, l_j), op(b.Qt, 1, 0, s2 * d, gq * qt_a, qt_a, 0, d),
+                 op(b.Ah, pd_k, 1, 0, gq * pd_a, pd_a, pd_c, d), 1.f, 0);
+            sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(Lp, b.cR, bh * pairs, (int)s2, (int)s1, 1.f);
+            normalize_rows<<<blocks_for(bh * pairs * d), 256, 0, stream>>>(b.Ah, b.cR, bh * pairs * d, (int)d,
+                                                                          g.eps_div);
+            At = b.Ah;
+            At_rows = op(b.Ah, d, 0, 1, gq * pd_a, pd_a, pd_c, pd_k);
+        }
+        // forward recompute: aL = R K (and Y = R V on the last refinement)   (M = j, N = e, K = i)
+        gemm(c, "bwd_alpha_l", (int)s2, (int)d, 1, (int)s2, nb_ack, op(R, s2, 0, 1, gq * r_a, r_a, r_c, r_k),
+             op(b.Kt, 1, 0, d, gk * kt_c, 0, kt_c, s2 * d), op(b.aL, d, 1, 0, gq * pd_a, pd_a, pd_c, pd_k), 1.f, 0);
+        if (last) {
+            gemm(c, "bwd_y", (int)s2, (int)dv, 1, (int)s2, nb_ack, op(R, s2, 0, 1, gq * r_a, r_a, r_c, r_k),
+                 op(b.Vt, 1, 0, dv, gk * vt_c, 0, vt_c, s2 * dv), op(b.Y, dv, 1, 0, gq * pv_a, pv_a, pv_c, pv_k), 1.f,
+                 0);
+            // dL[a][c][j][l][k] = dO[a][l][j][:] . Y[a][c][k][j][:]   (M = l, N = k, K = e)
+            gemm(c, "bwd_dl", (int)s1, (int)s1, 1, (int)dv, nb_acj, op(b.dOt, s2 * dv, 0, 1, gq * do_a, do_a, 0, dv),
+                 op(b.Y, pv_k, 0, 1, gq * pv_a, pv_a, pv_c, dv), op(b.dL, s1, 1, 0, gq * l_a, l_a, l_c, l_j), 1.f, 0);
+        }
+        // dS = L (dL - sum L dL)
+        softmax_bwd_cols<<<blocks_for(bha * s2 * s1 * 32), 256, 0, stream>>>(L, b.dL, bha * s2 * s1, (int)gk, (int)s2,
+                                                                          (int)s1);
+        // dQ[a][l][j][:] += sum_(c,k) dS[a][c][j][l][k] aL[a][c][k][j][:]   (M = l, N = e, K = (c, k))
+        gemm(c, "bwd_dq_col", (int)s1, (int)d, (int)gk, (int)s1, nb_aj, op(b.dL, s1, l_c, 1, gq * l_a, l_a, 0, l_j),
+             op(b.aL, 1, pd_c, pd_k, gq * pd_a, pd_a, 0, d), op(b.dQt, s2 * d, 1, 0, gq * qt_a, qt_a, 0, d), 1.f, 1);
+        // daL[a][c][k][j][:] = sum_l dS[a][c][j][l][k] Q[a][l][j][:]   (M = k, N = e, K = l)
+        gemm(c, "bwd_dalpha_l", (int)s1, (int)d, 1, (int)s1, nb_acj, op(b.dL, 1, 0, s1, gq * l_a, l_a, l_c, l_j),
+             op(b.Qt, 1, 0, s2 * d, gq * qt_a, qt_a, 0, d), op(b.daL, pd_k, 1, 0, gq * pd_a, pd_a, pd_c, d), 1.f, 0);
+        // dc_L[a][c][k][j] = -sum_l dS
+        sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(b.dL, b.dcL, bh * pairs, (int)s2, (int)s1, -1.f);
+        if (last) {
+            // dY[a][c][k][j][:] = sum_l L[a][c][j][l][k] dO[a][l][j][:]
+            gemm(c, "bwd_dy", (int)s1, (int)dv, 1, (int)s1, nb_acj, op(L, 1, 0, s1, gq * l_a, l_a, l_c, l_j),
+                 op(b.dOt, 1, 0, s2 * dv, gq * do_a, do_a, 0, dv), op(b.dY, pv_k, 1, 0, gq * pv_a, pv_a, pv_c, dv), 1.f,
+                 0);
+        }
+        // z = A_t K^T  (M = j, N = i, K = e)
+        gemm(c, "bwd_z", (int)s2, (int)s2, 1, (int)d, nb_ack, At_rows, op(b.Kt, d, 0, 1, gk * kt_c, 0, kt_c, s2 * d),
+             op(b.z, s2, 1, 0, gq * r_a, r_a, r_c, r_k), 1.f, 0);
+        // dR = dY V^T (last) + daL K^T
+        if (last)
+            gemm(c, "bwd_dr_v", (int)s2, (int)s2, 1, (int)dv, nb_ack, op(b.dY, dv, 0, 1, gq * pv_a, pv_a, pv_c, pv_k),
+                 op(b.Vt, dv, 0, 1, gk * vt_c, 0, vt_c, s2 * dv), op(b.dR, s2, 1, 0, gq * r_a, r_a, r_c, r_k), 1.f, 0);
+        gemm(c, "bwd_dr_k", (int)s2, (int)s2, 1, (int)d, nb_ack, op(b.daL, d, 0, 1, gq * pd_a, pd_a, pd_c, pd_k),
+             op(b.Kt, d, 0, 1, gk * kt_c, 0, kt_c, s2 * d), op(b.dR, s2, 1, 0, gq * r_a, r_a, r_c, r_k), 1.f, last);
+        // dz (in place over dR)
+        softmax_bwd_rows<<<blocks_for(bh * pairs * 32), 256, 0, stream>>>(R, b.z, b.dR, b.dcL, bh * pairs, (int)s2);
+        // dK[c][k][i][:] += sum_(a,j) dz[a][c][k][j][i] A_t[a][c][k][j][:] + R daL   (M = i, N = e, K = (a, j))
+        {
+            Operand Ab = At_rows;   // as B[k1 = a][k2 = j][n = e]
+            Operand B_at = op(At, 1, Ab.b[1], Ab.s0, Ab.b[0], 0, Ab.b[2], Ab.b[3]);
+            gemm(c, "bwd_dk_z", (int)s2, (int)d, (int)gq, (int)s2, nb_ck, op(b.dR, 1, r_a, s2, gq * r_a, 0, r_c, r_k),
+                 B_at, op(b.dKt, d, 1, 0, gk * kt_c, 0, kt_c, s2 * d), 1.f, 1);
+        }
+        gemm(c, "bwd_dk_r", (int)s2, (int)d, (int)gq, (int)s2, nb_ck, op(R, 1, r_a, s2, gq * r_a, 0, r_c, r_k),
+             op(b.daL, 1, pd_a, d, gq * pd_a, 0, pd_c, pd_k), op(b.dKt, d, 1, 0, gk * kt_c, 0, kt_c, s2 * d), 1.f, 1);
+        if (last)
+            gemm(c, "bwd_dv", (int)s2, (int)dv, (int)gq, (int)s2, nb_ck, op(R, 1, r_a, s2, gq * r_a, 0, r_c, r_k),
+                 op(b.dY, 1, pv_a, dv, gq * pv_a, 0, pv_c, pv_k), op(b.dVt, dv, 1, 0, gk * vt_c, 0, vt_c, s2 * dv), 1.f,
+                 1);
+        if (t == 0) {
+            // dQ[a][k][j][:] += sum_(c,i) dz[a][c][k][j][i] K[c][k][i][:]   (M = j, N = e, K = (c, i))
+            gemm(c, "bwd_dq_row", (int)s2, (int)d, (int)gk, (int)s2, nb_ak, op(b.dR, s2, r_c, 1, gq * r_a, r_a, 0, r_k),
+                 op(b.Kt, 1, kt_c, d, gk * kt_c, 0, 0, s2 * d), op(b.dQt, d, 1, 0, gq * qt_a, qt_a, 0, s2 * d), 1.f,
+                 1);
+        } else {
+            // dA_t = dz K  -> dalpha_R, dc_R -> dL_{t-1}, dQ
+            gemm(c, "bwd_da", (int)s2, (int)d, 1, (int)s2, nb_ack, op(b.dR, s2, 0, 1, gq * r_a, r_a, r_c, r_k),
+                 op(b.Kt, 1, 0, d, gk * kt_c, 0, kt_c, s2 * d), op(b.dAh, d, 1, 0, gq * pd_a, pd_a, pd_c, pd_k), 1.f, 0);
+            normalize_bwd<<<blocks_for(bh * pairs * 32), 256, 0, stream>>>(b.dAh, b.Ah, b.cR, b.dcR, bh * pairs,
+                                                                          (int)d, g.eps_div);
+            const float* Lp = lf + (size_t)(t - 1) * bh * lsz;
+            // dL_{t-1}[a][c][j][l][k] = Q[a][l][j][:] . dalpha_R[a][c][k][j][:] + dc_R   (M = l, N = k, K = e)
+            gemm(c, "bwd_dl_prev", (int)s1, (int)s1, 1, (int)d, nb_acj, op(b.Qt, s2 * d, 0, 1, gq * qt_a, qt_a, 0, d),
+                 op(b.dAh, pd_k, 0, 1, gq * pd_a, pd_a, pd_c, d), op(b.dLp, s1, 1, 0, gq * l_a, l_a, l_c, l_j), 1.f, 0);
+            add_dcr<<<blocks_for(bh * lsz), 256, 0, stream>>>(b.dLp, b.dcR, bh * lsz, (int)s2, (int)s1);
+            // dQ[a][l][j][:] += sum_(c,k) L_{t-1}[a][c][j][l][k] dalpha_R[a][c][k][j][:]
+            gemm(c, "bwd_dq_alpha", (int)s1, (int)d, (int)gk, (int)s1, nb_aj, op(Lp, s1, l_c, 1, gq * l_a, l_a, 0, l_j),
+                 op(b.dAh, 1, pd_c, pd_k, gq * pd_a, pd_a, 0, d), op(b.dQt, s2 * d, 1, 0, gq * qt_a, qt_a, 0, d), 1.f,
+                 1);
+            float* tmp = b.dL;   // dL_{t-1} becomes the next step's dL
+            b.dL = b.dLp;
+            b.dLp = tmp;
+        }
+        if (c.err != cudaSuccess) return c.err;
+        if ((c.err = cudaGetLastError()) != cudaSuccess) return c.err;
+    }
+    // scatter back to token order: dq = scale * dQt (Q entered the solver as scale * q)
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dQt, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, dq_out);
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dKt, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, dk_out);
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dVt, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, dv_out);
+    (void)nb_ak;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t backward_workspace_bytes(const Geometry& g) { return layout(g, nullptr, nullptr); }
+
+cudaError_t backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
+                     const float* l_factors, const float* r_factors, void* dq, void* dk, void* dv, void* ws,
+                     cudaStream_t stream) {
+    if (dtype == MBX_F32)
+        return backward_t<float>(g, (const float*)q, (const float*)k, (const float*)v, (const float*)dout, l_factors,
+                                 r_factors, (float*)dq, (float*)dk, (float*)dv, (char*)ws, stream);
+    return backward_t<__nv_bfloat16>(g, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k, (const __nv_bfloat16*)v,
+                                     (const __nv_bfloat16*)dout, l_factors, r_factors, (__nv_bfloat16*)dq,
+                                     (__nv_bfloat16*)dk, (__nv_bfloat16*)dv, (char*)ws, stream);
+}
+
+}  // namespace mbx

@@ -160,8 +160,9 @@ row_stage(Geometry g, const T* __restrict__ q, const T* __restrict__ k, const T*
         if (lane == 0) ws.c_l[o] = A * inv_l - lse;   // sum_i R_i z_i - lse = sum R log R
     }
 
-    // Optional export of the final R' [l1,j1,k1,i1,k2,j2,i2] (factors.py:61-64).
-    if (!(last && r_factor)) return;
+    // Optional export of R' [l1,j1,k1,i1,k2,j2,i2] (factors.py:61-64): the final one, or this
+    // refinement's slice when every refinement is exported (MBX_FLAG_ALL_ITERS).
+    if (!r_factor) return;
     float* rrow = r_factor + (((((int64_t)bh * g.gq + a) * g.gk + c) * g.s1 + kr) * g.s2 + (jv ? j : 0)) * g.s2;
     for (int i0 = 0; i0 < g.s2; i0 += kChunk) {
         __syncthreads();
@@ -461,7 +462,7 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 template <typename T>
 cudaError_t forward_t(const Geometry& g, const T* q, const T* k, const T* v, T* out,
-                      float* l_factor, float* r_factor, const Workspace& ws, cudaStream_t st) {
+                      float* l_factor, float* r_factor, const Workspace& ws, cudaStream_t st, bool all_iters) {
     const size_t sm_row = sizeof(float) * (kChunk * (g.d + 1) + kChunk * (g.dv + 1) + kWarps * g.d);
     const size_t sm_col = sizeof(float) * (kChunk * (g.d + 1) + kChunk * (g.dv + 1) + kChunk + kWarps * g.d);
     const size_t sm_ar = sizeof(float) * (kChunk * (g.d + 1) + kChunk + kWarps * g.d);
@@ -472,19 +473,23 @@ cudaError_t forward_t(const Geometry& g, const T* q, const T* k, const T* v, T* 
     const dim3 grid_row(g.gq * g.gk * g.s1, cdiv(g.s2, kWarps), g.bh);
     const dim3 grid_col(g.gq * g.s2, cdiv(g.s1, kWarps), g.bh);
     const dim3 grid_ar(g.gq * g.s2, cdiv(g.nkeys, kWarps), g.bh);
+    const size_t rslice = (size_t)g.bh * g.gq * g.gk * g.s1 * g.s2 * g.s2;
+    const size_t lslice = (size_t)g.bh * g.gq * g.gk * g.s2 * g.s1 * g.s1;
     for (int it = 0; it < g.T; ++it) {
         const int last = it == g.T - 1;
+        float* rf = !r_factor ? nullptr : all_iters ? r_factor + it * rslice : last ? r_factor : nullptr;
+        float* lf = !l_factor ? nullptr : all_iters ? l_factor + it * lslice : last ? l_factor : nullptr;
         {
             ProfScope p("simt_row_stage", st);
-            row_stage<T><<<grid_row, kThreads, sm_row, st>>>(g, q, k, v, ws, it, last, r_factor);
+            row_stage<T><<<grid_row, kThreads, sm_row, st>>>(g, q, k, v, ws, it, last, rf);
         }
         {
             ProfScope p("simt_column_stage", st);
             column_stage<T><<<grid_col, kThreads, sm_col, st>>>(g, q, last ? out : nullptr, ws, last);
         }
-        if (!last || l_factor) {
+        if (!last || lf) {
             ProfScope p("simt_alpha_r_stage", st);
-            alpha_r_stage<T><<<grid_ar, kThreads, sm_ar, st>>>(g, q, ws, last ? 0 : 1, last ? l_factor : nullptr);
+            alpha_r_stage<T><<<grid_ar, kThreads, sm_ar, st>>>(g, q, ws, last ? 0 : 1, lf);
         }
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
@@ -507,13 +512,13 @@ cudaError_t apply_t(const Geometry& g, const float* l_factor, const float* r_fac
 
 cudaError_t generic_forward(const Geometry& g, int dtype, const void* q, const void* k,
                             const void* v, void* out, float* l_factor, float* r_factor,
-                            const Workspace& ws, cudaStream_t stream) {
+                            const Workspace& ws, cudaStream_t stream, bool all_iters) {
     if (dtype == MBX_F32)
         return forward_t<float>(g, (const float*)q, (const float*)k, (const float*)v, (float*)out,
-                                l_factor, r_factor, ws, stream);
+                                l_factor, r_factor, ws, stream, all_iters);
     return forward_t<__nv_bfloat16>(g, (const __nv_bfloat16*)q, (const __nv_bfloat16*)k,
                                     (const __nv_bfloat16*)v, (__nv_bfloat16*)out, l_factor,
-                                    r_factor, ws, stream);
+                                    r_factor, ws, stream, all_iters);
 }
 
 cudaError_t generic_apply(const Geometry& g, int dtype, const float* l_factor,

@@ -66,7 +66,7 @@ struct ProfScope {
 // SIMT kernels (mbx_generic.cu) -- any plan, fp32 or bf16 I/O.
 cudaError_t generic_forward(const Geometry& g, int dtype, const void* q, const void* k,
                             const void* v, void* out, float* l_factor, float* r_factor,
-                            const Workspace& ws, cudaStream_t stream);
+                            const Workspace& ws, cudaStream_t stream, bool all_iters = false);
 cudaError_t generic_apply(const Geometry& g, int dtype, const float* l_factor,
                           const float* r_factor, const void* v, void* out,
                           const Workspace& ws, cudaStream_t stream);
@@ -93,5 +93,11 @@ size_t tc_workspace_bytes(const Geometry& g, int flags);
 cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* k, const void* v,
                        void* out, float* l_factor, float* r_factor, void* workspace,
                        cudaStream_t stream);
+
+// Backward pass (mbx_backward.cu): dq, dk, dv from dout and the factors of every refinement.
+size_t backward_workspace_bytes(const Geometry& g);
+cudaError_t backward(const Geometry& g, int dtype, const void* q, const void* k, const void* v, const void* dout,
+                     const float* l_factors, const float* r_factors, void* dq, void* dk, void* dv, void* ws,
+                     cudaStream_t stream);
 
 }  // namespace mbx

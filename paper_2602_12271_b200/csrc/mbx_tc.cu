@@ -152,8 +152,18 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base, 
     EncodeTiledFn enc = encode_fn();
     if (!enc) return false;
     cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    return enc(m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const CUresult r = enc(m, dt, rank, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS && getenv("MBX_VERBOSE")) {
+        fprintf(stderr, "mbx: cuTensorMapEncodeTiled failed (%d): base %p rank %d dims", (int)r, base, rank);
+        for (int i = 0; i < rank; ++i) fprintf(stderr, " %llu", (unsigned long long)dims[i]);
+        fprintf(stderr, " strides");
+        for (int i = 0; i + 1 < rank; ++i) fprintf(stderr, " %llu", (unsigned long long)strides[i]);
+        fprintf(stderr, " box");
+        for (int i = 0; i < rank; ++i) fprintf(stderr, " %u", box[i]);
+        fprintf(stderr, "\n");
+    }
+    return r == CUDA_SUCCESS;
 }
 
 // (B, H, N, 128) bf16 with element strides st[b,h,token]; box (64 features, rows tokens).
@@ -524,8 +534,9 @@ static cudaError_t ensure_attributes(int dev) {
     return cudaSuccess;
 }
 
-static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void* k, const void* v, void* out,
-                                  float* l_factor, float* r_factor, void* workspace, int dev, cudaStream_t stream) {
+static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, const void* k, const void* v,
+                                  void* out, float* l_factor, float* r_factor, void* workspace, int dev,
+                                  cudaStream_t stream) {
     cudaError_t e = ensure_attributes(dev);
     if (e != cudaSuccess) return e;
     TcPlan T;
@@ -557,42 +568,50 @@ static cudaError_t tc_forward_one(const Geometry& g0, const void* q, const void*
                     cudaGetErrorString(le));
         return le;
     };
-    auto column = [&](int mode) -> cudaError_t {
+    auto column = [&](int mode, TcParams& Pc) -> cudaError_t {
         if (T.wide) {
             ProfScope p("tc_column_wide", stream);
-            void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+            void* args[] = {(void*)&Pc, (void*)&g, (void*)&mode};
             return launch((const void*)tc_column_wide, T.grid_wide, kWideThreads, T.smem_wide, args);
         }
         ProfScope p("tc_column_stage", stream);
-        void* args[] = {(void*)&P, (void*)&g, (void*)&mode};
+        void* args[] = {(void*)&Pc, (void*)&g, (void*)&mode};
         return launch((const void*)tc_column_stage, T.grid_col, kColThreads, T.smem_col, args);
     };
-    auto alpha = [&](int amode) -> cudaError_t {
+    auto alpha = [&](int amode, TcParams& Pc) -> cudaError_t {
         ProfScope p(amode ? "tc_alpha_l_export" : "tc_alpha_r_stage", stream);
-        void* args[] = {(void*)&P, (void*)&g, (void*)&amode};
+        void* args[] = {(void*)&Pc, (void*)&g, (void*)&amode};
         return launch((const void*)tc_alpha_r_stage, T.grid_alpha, kAlphaThreads, T.smem_alpha, args);
     };
     // refinements (solver.py:184-195): row stage (A = Q at t = 0, hat_alpha_R after), then either
     // the L statistics + alpha_R hand-off (t < T-1) or the output O = L Y (t = T-1).  With factor
     // export the last refinement also runs the statistics pass and writes L' from it
-    // (factors.py:57-79 layout); R' comes from the last row stage's softmax.
+    // (factors.py:57-79 layout); R' comes from the last row stage's softmax.  With
+    // MBX_FLAG_ALL_ITERS every refinement t writes slice t of both factors (the backward pass).
+    const bool all_iters = (flags & MBX_FLAG_ALL_ITERS) != 0;
+    const size_t rslice = (size_t)g0.bh * g.gq * g.gk * g.s1 * g.s2 * g.s2;
+    const size_t lslice = (size_t)g0.bh * g.gq * g.gk * g.s2 * g.s1 * g.s1;
+    TcParams Pt = P;   // per-refinement copy: factor slices
     for (int t = 0; t < g.T; ++t) {
         int last = t == g.T - 1, amode = t > 0;
+        Pt.rfac = !r_factor ? nullptr : all_iters ? r_factor + t * rslice : last ? r_factor : nullptr;
+        Pt.lfac = !l_factor ? nullptr : all_iters ? l_factor + t * lslice : last ? l_factor : nullptr;
         if (T.pair) {
             ProfScope p("tc_row_pair", stream);
-            void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
-            if ((e = launch((const void*)tc_row_pair, T.grid_pair, kPairThreads, T.smem_pair, args)) != cudaSuccess) return e;
+            void* args[] = {(void*)&Pt, (void*)&g, (void*)&amode, (void*)&last};
+            if ((e = launch((const void*)tc_row_pair, T.grid_pair, kPairThreads, T.smem_pair, args)) != cudaSuccess)
+                return e;
         } else {
             ProfScope p("tc_row_stage", stream);
-            void* args[] = {(void*)&P, (void*)&g, (void*)&amode, (void*)&last};
+            void* args[] = {(void*)&Pt, (void*)&g, (void*)&amode, (void*)&last};
             if ((e = launch((const void*)tc_row_stage, T.grid_row, kRowThreads, T.smem_row, args)) != cudaSuccess)
                 return e;
         }
         if (!last) {
-            if ((e = column(1)) != cudaSuccess || (e = alpha(0)) != cudaSuccess) return e;
+            if ((e = column(1, Pt)) != cudaSuccess || (e = alpha(0, Pt)) != cudaSuccess) return e;
         } else {
-            if (factors && l_factor && ((e = column(1)) != cudaSuccess || (e = alpha(1)) != cudaSuccess)) return e;
-            if ((e = column(0)) != cudaSuccess) return e;
+            if (Pt.lfac && ((e = column(1, Pt)) != cudaSuccess || (e = alpha(1, Pt)) != cudaSuccess)) return e;
+            if ((e = column(0, Pt)) != cudaSuccess) return e;
         }
     }
     return cudaGetLastError();
@@ -673,6 +692,14 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
+    // The tensor-map encode is a driver call: it needs the device's primary context current on
+    // this thread, which a thread that has only made runtime calls that do not touch the context
+    // (e.g. PyTorch's autograd worker) may not have yet.  cudaSetDevice binds it (once per thread).
+    thread_local int bound_dev = -1;
+    if (bound_dev != dev) {
+        if ((e = cudaSetDevice(dev)) != cudaSuccess) return e;
+        bound_dev = dev;
+    }
     const bool factors = l_factor || r_factor;
     SideStream* ss = nullptr;
     if (!factors && tc_split(g, flags)) {
@@ -683,7 +710,7 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
     }
     if (!ss) {
         Geometry g1 = g;
-        return tc_forward_one(g1, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
+        return tc_forward_one(g1, flags, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
     }
     const Geometry h = half_heads(g);
     const size_t wsh = align256(tc_layout(h).total);
@@ -693,8 +720,8 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
     };
     if ((e = cudaEventRecord(ss->fork, stream)) != cudaSuccess || (e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess)
         return e;
-    cudaError_t e1 = tc_forward_one(h, q, k, v, out, nullptr, nullptr, workspace, dev, stream);
-    cudaError_t e2 = tc_forward_one(h, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
+    cudaError_t e1 = tc_forward_one(h, flags, q, k, v, out, nullptr, nullptr, workspace, dev, stream);
+    cudaError_t e2 = tc_forward_one(h, flags, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
                                     nullptr, nullptr, reinterpret_cast<char*>(workspace) + wsh, dev, ss->side);
     // the join is recorded even if a half failed, so the side stream never dangles outside a capture
     if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess || (e = cudaStreamWaitEvent(stream, ss->join, 0)) != cudaSuccess)

@@ -168,7 +168,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             const uint32_t prow = smem_u32(base + AlphaSmem::kP) + r * 128;
             // L' row of this key: [bh][a][c][j][l][k] with key = c s1 + k
             float* lrow = nullptr;
-            if (lexp && key_ok) {
+            if (P.lfac && key_ok) {
                 const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
                 const int c = key / g.s1, kk = key - c * g.s1;
                 lrow = P.lfac + ((((int64_t)(bh * g.gq + a) * g.gk + c) * g.s2 + j) * g.s1) * g.s1 + kk;
@@ -184,14 +184,12 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
                     p[i] = (l < g.s1 && key_ok) ? e : 0.f;
                     cr += p[i];
                 }
-                if (lexp) {
-                    if (lrow) {
+                if (lrow) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (l0 + i < g.s1) lrow[(int64_t)(l0 + i) * g.s1] = p[i];
-                    }
-                    continue;
+                    for (int i = 0; i < 32; ++i)
+                        if (l0 + i < g.s1) lrow[(int64_t)(l0 + i) * g.s1] = p[i];
                 }
+                if (lexp) continue;
                 // P^T row (keys on rows, l along K): 64-l chunk l0 / 64, logical 16 B chunks (l0 % 64) / 8 ..
                 const uint32_t pr = prow + (l0 >> 6) * 16384;
 #pragma unroll

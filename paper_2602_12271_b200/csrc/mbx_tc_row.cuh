@@ -494,7 +494,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
             tmem_st32(sbuf, reinterpret_cast<const float*>(packed));
             tc_fence_before();
             mbar_arrive(&p_full[bsel]);
-            if (P.rfac && want_y && row_ok)   // final R' row [bh][a][c][k][j][:] (factors.py:57-79)
+            if (P.rfac && row_ok)   // R' row (final, or this refinement's slice) [bh][a][c][k][j][:] (factors.py:57-79)
                 store_r_row(P.rfac + ((((int64_t)(cur.bh * g.gq + kQG * cur.qg + al) * g.gk + cur.c) * g.s1 + cur.kr) *
                                           g.s2 + j) * g.s2,
                             p, inv_l, g.s2);

@@ -393,7 +393,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 tc_fence_before();
                 mbar_arrive(&p_full[bsel]);
                 if (lane == 0) TR(warp, ti, 22);
-                if (P.rfac && want_y && row_ok)   // final R' row [bh][a][c][k][j][:] (factors.py:57-79)
+                if (P.rfac && row_ok)   // R' row (final, or this refinement's slice) [bh][a][c][k][j][:] (factors.py:57-79)
                     store_r_row(P.rfac + ((((int64_t)(cur.bh * g.gq + qt) * g.gk + cur.c) * g.s1 + kr) * g.s2 + j) * g.s2,
                                 z, inv_l, g.s2);
                 if (row_ok) {   // c_L = sum R z - lse with z = scale * S (solver.py:191)

@@ -158,9 +158,11 @@ def _workspace(device: torch.device, stream, nbytes: int) -> torch.Tensor:
 
 
 def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_log=1e-300,
-            out=None, return_factors=False, force_generic=False, workspace=None, split=None):
+            out=None, return_factors=False, force_generic=False, workspace=None, split=None,
+            all_iters=False):
     """Run ``mbx_forward``; returns out or (out, L', R') with fp32 factors of
-    shape (B, H, c1_q, c2, c1_kv, c2, s2, s1, s1) / (..., s1, s2, s2).
+    shape (B, H, c1_q, c2, c1_kv, c2, s2, s1, s1) / (..., s1, s2, s2) -- with
+    ``all_iters`` one such slice per refinement, stacked on a leading T axis.
 
     ``split``: None = the library's choice of concurrent head halves, True / False
     force it on / off.  The call is enqueued on the current stream of q's device
@@ -171,15 +173,18 @@ def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_
     flags = _lib.FLAG_FORCE_GENERIC if force_generic else 0
     if return_factors:
         flags |= _lib.FLAG_FACTORS
+        if all_iters:
+            flags |= _lib.FLAG_ALL_ITERS
     if split is not None:
         flags |= _lib.FLAG_SPLIT if split else _lib.FLAG_NO_SPLIT
     prep, nbytes = _prepared(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags)
     lf = rf = None
     if return_factors:
         B, H = q.shape[:2]
-        lf = torch.empty((B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s2, low.s1, low.s1),
+        lead = (iterations,) if all_iters else ()
+        lf = torch.empty(lead + (B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s2, low.s1, low.s1),
                          dtype=torch.float32, device=q.device)
-        rf = torch.empty((B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s1, low.s2, low.s2),
+        rf = torch.empty(lead + (B, H, low.c1_q, low.c2, low.c1_kv, low.c2, low.s1, low.s2, low.s2),
                          dtype=torch.float32, device=q.device)
     with torch.cuda.device(q.device):
         stream = torch.cuda.current_stream(q.device).cuda_stream
@@ -197,6 +202,45 @@ def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_
     if return_factors:
         return out, lf, rf
     return out
+
+
+def backward(q, k, v, dout, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_log=1e-300,
+             factors=None):
+    """Gradients (dq, dk, dv) of sum(out * dout) through ``mbx_backward``.
+
+    ``factors`` = (L', R') of every refinement as returned by
+    ``forward(..., return_factors=True, all_iters=True)``; recomputed when absent
+    (FlashAttention-style recomputation: the forward is cheap next to the backward)."""
+    lib = _lib.load()
+    if factors is None:
+        _, lf, rf = forward(q, k, v, low, iterations, scale, eps_div, eps_log, return_factors=True,
+                            all_iters=True)
+    else:
+        lf, rf = factors
+    dout = dout.to(q.dtype)
+    if dout.stride(-1) != 1:
+        dout = dout.contiguous()
+    prep = prepare(q, k, v, dout, low, iterations, scale, eps_div, eps_log)
+    try:
+        _lib.check(lib.mbx_validate(ctypes.byref(prep.desc)))
+    except _lib.MbxError as e:
+        _raise_mapped(e)
+    dq, dk, dv = (torch.empty_like(x) for x in (q, k, v))
+    if tuple(dq.stride()) != tuple(q.stride()) or tuple(dk.stride()) != tuple(k.stride()) or \
+            tuple(dv.stride()) != tuple(v.stride()):
+        raise SolverError("gradient tensors must share the strides of q, k, v")
+    nbytes = lib.mbx_backward_workspace_bytes(ctypes.byref(prep.desc))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=q.device)
+    with torch.cuda.device(q.device):
+        st = lib.mbx_backward(ctypes.byref(prep.desc), q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(),
+                              lf.data_ptr(), rf.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                              ws.data_ptr(), nbytes, torch.cuda.current_stream(q.device).cuda_stream)
+    if st != 0:
+        try:
+            _lib.check(st)
+        except _lib.MbxError as e:
+            _raise_mapped(e)
+    return dq, dk, dv
 
 
 def apply(l_factor: torch.Tensor, r_factor: torch.Tensor, v: torch.Tensor, low: Lowered,
@@ -266,6 +310,21 @@ def _monarch_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: str, it
 @_monarch_op.register_fake
 def _monarch_op_fake(q, k, v, plan, iterations, scale):
     return q.new_empty(q.shape[:3] + (v.shape[3],))
+
+
+def _op_setup_context(ctx, inputs, output):
+    q, k, v, plan, iterations, scale = inputs
+    ctx.save_for_backward(q, k, v)
+    ctx.plan, ctx.iterations, ctx.scale = plan, iterations, scale
+
+
+def _op_backward(ctx, dout):
+    q, k, v = ctx.saved_tensors
+    dq, dk, dv = backward(q, k, v, dout, _LOWERED[ctx.plan], ctx.iterations, ctx.scale)
+    return dq, dk, dv, None, None, None
+
+
+_monarch_op.register_autograd(_op_backward, setup_context=_op_setup_context)
 
 
 def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = None,
@@ -359,6 +418,6 @@ def monarch_attention_host(q, k, v, plan, iterations: int = 1, scale: float | No
     return out
 
 
-__all__ = ["monarch_attention", "monarch_attention_host", "forward", "apply", "prepare", "selected_path",
+__all__ = ["monarch_attention", "monarch_attention_host", "forward", "backward", "apply", "prepare", "selected_path",
            "lower_for", "plan_key",
            "SolverError", "BlockConfig", "TilePlan"]
