@@ -621,6 +621,48 @@ def run_ours(args):
                  "overhead_us_above_device": round(max(0.0, (t2 - t0) * 1e6 / n_calls - dev_ms * 1e3), 2),
                  "calls": n_calls, "api": "paper_2602_12271_b200.monarch_attention (device tensors)"}
 
+    # ---- backward pass (finetuning step): forward recompute with factor export + mbx_backward ----
+    bwd = None
+    if not strong and not args.no_backward:
+        dout = torch.randn(out.shape, device=dev, dtype=dtype, generator=g)
+
+        def bwd_step():
+            ops.backward(q, k, v, dout, low, wl["T"])
+
+        bwd_step()
+        torch.cuda.synchronize()
+        bsteps = max(3, min(args.steps, 10))
+        bwd_ms = D.max(time_steps(bwd_step, bsteps, 2, flush, stream)) / bsteps
+        lib.mbx_profile_enable(1)
+        flush()
+        bwd_step()
+        torch.cuda.synchronize()
+        lib.mbx_profile_enable(0)
+        brecs = _lib.profile_collect_ex()
+        bk = {}
+        for nm, _, ms in brecs:
+            bk[nm] = bk.get(nm, 0.0) + ms
+        dense_bwd = None
+        if rank == 0 and not args.no_dense:
+            try:
+                from torch.nn.attention import SDPBackend, sdpa_kernel
+
+                qd, kd, vd = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+
+                def dense_bwd_step():
+                    with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                        o_ = torch.nn.functional.scaled_dot_product_attention(qd, kd, vd)
+                    o_.backward(dout)
+
+                dense_bwd_step()
+                torch.cuda.synchronize()
+                dense_bwd = round(time_steps(dense_bwd_step, bsteps, 2, flush, stream) / bsteps, 5)
+            except Exception as e:   # backend unavailable
+                dense_bwd = f"unavailable: {type(e).__name__}"
+        bwd = {"ms": round(bwd_ms, 5), "includes": "forward recompute with factor export + mbx_backward",
+               "dense_fwd_plus_bwd_ms_cudnn": dense_bwd, "arith": "fp32 SIMT (batched GEMM chain)",
+               "kernels_ms": {kk: round(vv, 5) for kk, vv in sorted(bk.items(), key=lambda x: -x[1])[:8]}}
+
     # ---- end-to-end through the public API with host buffers ----
     # monarch_attention_host: pinned host q/k/v in, host output back, H2D / forward / D2H
     # pipelined over (b,h) chunks (all inside the timed region), once per layer of the step
@@ -697,7 +739,7 @@ def run_ours(args):
             "kernels": kernels, "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 5), "unit": unit, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "api": "paper_2602_12271_b200.monarch_attention_host"},
-            "eager": eager, "allgather": allgather,
+            "eager": eager, "allgather": allgather, "backward": bwd,
             "gpu_launches": int(round(launches_per_layer * layers * args.steps)),
             "clocks": clk.summary(),
         }
@@ -738,6 +780,7 @@ def main():
     ap.add_argument("--iters", type=int, default=1)
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-backward", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
