@@ -457,24 +457,33 @@ class _Dist:
 
 
 def _merge_stages(recs, steps):
-    """Per-stage device time per step from per-launch (name, start, ms) records: the
-    launches of one stage inside a step (e.g. the two concurrent halves on two
-    streams) are merged into one span [first start, last end] carrying the stage's
-    whole work, so shares and roofline use whole-stage work over whole-stage time."""
+    """Per-stage device time per step from per-launch (name, start, ms) records.  Launches of
+    one stage that overlap in time (the two concurrent halves on two streams) are merged
+    into one span [first start, last end] carrying the whole stage's work; sequential
+    launches of a stage (one per refinement) are summed.  Shares and the roofline then
+    use whole-stage work over whole-stage time."""
     per_step = len(recs) // max(steps, 1)
     stages = {}
     for sidx in range(steps):
         chunk = recs[sidx * per_step:(sidx + 1) * per_step]
-        spans = {}
+        spans = {}   # name -> list of [lo, hi, launches]
         for name, st, ms in chunk:
-            lo, hi, n = spans.get(name, (st, st + ms, 0))
-            spans[name] = (min(lo, st), max(hi, st + ms), n + 1)
-        for name, (lo, hi, n) in spans.items():
-            stages.setdefault(name, []).append((hi - lo, n))
+            lst = spans.setdefault(name, [])
+            for sp in lst:
+                if st < sp[1] and st + ms > sp[0]:   # overlaps an open span of this stage
+                    sp[0], sp[1], sp[2] = min(sp[0], st), max(sp[1], st + ms), sp[2] + 1
+                    break
+            else:
+                lst.append([st, st + ms, 1])
+        for name, lst in spans.items():
+            stages.setdefault(name, []).append((sum(hi - lo for lo, hi, _ in lst), sum(n for _, _, n in lst),
+                                                len(lst)))
     out = []
     for name, vals in stages.items():
-        out.append({"name": name, "ms_avg": round(sum(v for v, _ in vals) / len(vals), 5),
-                    "launches_per_step": sum(n for _, n in vals) / len(vals), "stage_spans_per_step": 1})
+        nv = len(vals)
+        out.append({"name": name, "ms_avg": round(sum(v for v, _, _ in vals) / nv, 5),
+                    "launches_per_step": sum(n for _, n, _ in vals) / nv,
+                    "stage_spans_per_step": sum(k for _, _, k in vals) / nv})
     return out, per_step
 
 

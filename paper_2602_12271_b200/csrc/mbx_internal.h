@@ -81,6 +81,7 @@ struct Options {
     int wide = 0;       // 1: FlashAttention-style column stage for s1 <= 32 too (T = 1)
     int split = -1;     // concurrent halves: 0 off, 1 on
     int verbose = 0;    // print why a problem leaves the tcgen05 path / setup failures
+    int fusedhand = 1;  // T >= 2: alpha_R hand-off inside the column stage when a column is one key chunk
     unsigned version = 0;   // bumped on every change (keys the launch-parameter cache)
 };
 const Options& options();

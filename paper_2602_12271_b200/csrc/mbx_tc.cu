@@ -240,6 +240,7 @@ static void init_options() {
     g_opts.wide = env("MBX_WIDE", 0);
     g_opts.split = env("MBX_SPLIT", -1);
     g_opts.verbose = env("MBX_VERBOSE", 0);
+    g_opts.fusedhand = env("MBX_FUSEDHAND", 1);
 }
 
 const Options& options() {
@@ -254,7 +255,7 @@ int set_option(const char* name, int value) {
     struct { const char* n; int* p; } tab[] = {
         {"MBX_PDL", &g_opts.pdl}, {"MBX_L2HINT", &g_opts.l2hint}, {"MBX_DBG", &g_opts.dbg},
         {"MBX_PAIR", &g_opts.pair}, {"MBX_WIDE", &g_opts.wide}, {"MBX_SPLIT", &g_opts.split},
-        {"MBX_VERBOSE", &g_opts.verbose}};
+        {"MBX_VERBOSE", &g_opts.verbose}, {"MBX_FUSEDHAND", &g_opts.fusedhand}};
     for (auto& t : tab)
         if (strcmp(t.n, name) == 0) {
             const int prev = *t.p;
@@ -327,6 +328,7 @@ struct TcPlan {
     TcParams P;
     Geometry g;            // identity plans rewritten as a (1, s1, s2) neighborhood grid
     bool pair, wide;
+    bool fused_hand;       // T >= 2 hand-off fused into the stacked column stage (mode 2)
     int grid_pair, grid_row, grid_col, grid_wide, grid_alpha;
     int smem_row, smem_col, smem_pair, smem_wide, smem_alpha;
 };
@@ -437,6 +439,7 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
     const int sms = num_sms(dev);
     T->g = g;
     T->wide = wide;
+    T->fused_hand = !wide && g.T > 1 && g.nkeys <= kKC && o.fusedhand != 0;
     T->smem_row = RowSmem::kTotal + 1024;
     T->smem_col = ColSmem::kTotal + 1024;
     T->smem_alpha = AlphaSmem::kTotal + 1024;
@@ -608,7 +611,11 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
                 return e;
         }
         if (!last) {
-            if ((e = column(1, Pt)) != cudaSuccess || (e = alpha(0, Pt)) != cudaSuccess) return e;
+            if (T.fused_hand) {   // one key chunk per column: hand-off inside the column stage
+                if ((e = column(2, Pt)) != cudaSuccess) return e;
+            } else if ((e = column(1, Pt)) != cudaSuccess || (e = alpha(0, Pt)) != cudaSuccess) {
+                return e;
+            }
         } else {
             if (Pt.lfac && ((e = column(1, Pt)) != cudaSuccess || (e = alpha(1, Pt)) != cudaSuccess)) return e;
             if ((e = column(0, Pt)) != cudaSuccess) return e;

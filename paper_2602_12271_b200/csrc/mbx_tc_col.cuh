@@ -32,9 +32,17 @@ struct ColSmem {
 // Column-stage role of CTA `first` among `stride` column CTAs.
 // mode 0: O = L Y (last refinement); mode 1 (T >= 2, earlier refinements): only the
 // per-row softmax statistics (running max, sum) of L, for the alpha_R stage.
+// mode 2 (T >= 2, earlier refinements, all keys of a column in one 96-key chunk): the
+// alpha_R hand-off fused in (solver.py:185-186 of the next refinement): the softmax is
+// exact in one pass, so P_i = L (normalised, bf16) goes to shared memory and
+//     MMA_A_i  alpha_R_i[key, v] = P_i^T . Q_col_i      M=128 keys, N=128, K=32 rows l
+// runs into TMEM (D_i at columns 128 i, over the consumed S regions); c_R = sum_l L is a
+// warp transpose-reduce of the fp32 L row; the epilogue writes hat_alpha_R = alpha_R /
+// max(c_R, eps) (bf16) for the next row stage -- no statistics pass, no alpha_R stage.
 __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
                                          int mode = 0) {
     const bool outm = mode == 0;
+    const bool hand = mode == 2;
     const CUtensorMap& tm_w = P.tw;
     const CUtensorMap& tm_c = P.tc;
     const CUtensorMap& tm_qc = P.tqc;
@@ -231,9 +239,11 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 next_slot();
             }
         };
+        const uint32_t idesc_a = idesc_bf16(128, 128, true, true);   // A = P^T (MN-major), B = Q_col (MN-major)
         for (int u = 0; u < U; ++u) {
             const int gi = u / nch, ch = u - gi * nch;
             if (ch == 0) mbar_wait(q_full, gi & 1);
+            if (hand && gi > 0) mbar_wait(o_free, (gi - 1) & 1);   // D_i (over the S regions) drained
             for (int i = 0; i < 4; ++i) {
                 mbar_wait(&ring_full[slot], sph);
                 if (u > 0) mbar_wait(&s_free[i], (u - 1) & 1);
@@ -250,6 +260,24 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 }
                 __syncwarp();
                 next_slot();
+            }
+            if (hand) {   // nch == 1: alpha_R_i = P_i^T Q_col_i once every softmax wrote its P_i
+                // (D_i spans S regions of other columns: all four must have been read first)
+                for (int i = 0; i < 4; ++i) mbar_wait(&p_full[i], u & 1);
+                tc_fence_after();
+                for (int i = 0; i < 4; ++i) {
+                    if (leader) {
+                        const uint32_t pa = p_lo + (uint32_t)i * (8192 >> 4);   // [32 l][64 keys] x 2 key chunks
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)   // K = 32 rows l: two k-steps of 16 rows (2 KB)
+                            mma_bf16(tmem + i * 128,
+                                     desc((pa & ~(0x3FFFu << 16)) + ((kk * 2048) >> 4) + ((4096u >> 4) << 16)),
+                                     desc((q_lo & ~(0x3FFFu << 16)) + ((i * 4096 + kk * 2048) >> 4) + ((16384u >> 4) << 16)),
+                                     idesc_a, kk > 0);
+                        mma_commit(&o_done[i]);
+                    }
+                    __syncwarp();
+                }
             }
             if (ch == nch - 1) {
                 if (leader) mma_commit(q_empty);
@@ -316,6 +344,61 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     need = 1;
                 }
                 s_run *= fac;
+                if (hand) {   // one chunk: exact softmax, normalised P_i, c_R, optional L' export
+                    float sq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int k = 0; k < kKC; ++k) {
+                        x[k] = ex2(x[k] - m_run);
+                        sq[k & 3] += x[k];
+                    }
+                    const float inv = 1.f / ((sq[0] + sq[1]) + (sq[2] + sq[3]));
+                    const bool lrow = l < g.s1 && j0 + quad < g.s2;
+#pragma unroll
+                    for (int k = 0; k < kKC; ++k) x[k] = lrow ? x[k] * inv : 0.f;
+                    if (u > 0) mbar_wait(&o_done[quad], (u - 1) & 1);   // MMA_A_i(u-1) done with P_i
+#pragma unroll
+                    for (int cc = 0; cc < kKC / 8; ++cc) {
+                        const uint32_t dst = sP + (cc >> 3) * 4096 + l * 128 + (((cc & 7) ^ (l & 7)) << 4);
+                        st_shared_v4(dst, pack_bf16(x[cc * 8], x[cc * 8 + 1]), pack_bf16(x[cc * 8 + 2], x[cc * 8 + 3]),
+                                     pack_bf16(x[cc * 8 + 4], x[cc * 8 + 5]), pack_bf16(x[cc * 8 + 6], x[cc * 8 + 7]));
+                    }
+                    fence_proxy_async_smem();
+                    mbar_arrive(&p_full[quad]);
+                    if (P.lfac && lrow) {   // L'[bh][a][c][j][l][k], key = c s1 + k
+                        const int j = j0 + quad;
+                        float* lrow0 = P.lfac + ((((int64_t)(bh * g.gq + a) * g.gk) * g.s2 + j) * g.s1 + l) * g.s1;
+                        const int64_t cstride = (int64_t)g.s2 * g.s1 * g.s1;
+                        int c = 0, kk = 0;
+#pragma unroll
+                        for (int key = 0; key < kKC; ++key) {   // constant indices keep x in registers
+                            if (key < kvalid) lrow0[c * cstride + kk] = x[key];
+                            if (++kk == g.s1) {
+                                kk = 0;
+                                ++c;
+                            }
+                        }
+                    }
+                    // c_R[key] = sum_l L[l, key]: transpose-reduce over the warp, 32 keys per pass
+                    float* crs = reinterpret_cast<float*>(smem + ColSmem::kOut + 16384) + quad * 128;
+#pragma unroll
+                    for (int pass = 0; pass < kKC / 32; ++pass) {
+                        float v[32];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) v[e] = x[pass * 32 + e];
+#pragma unroll
+                        for (int sh = 16; sh >= 1; sh >>= 1) {
+#pragma unroll
+                            for (int e = 0; e < sh; ++e) {
+                                const bool up = (lane & sh) != 0;
+                                const float send = up ? v[e] : v[e + sh];
+                                const float keep = up ? v[e + sh] : v[e];
+                                v[e] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+                            }
+                        }
+                        crs[pass * 32 + lane] = v[0];
+                    }
+                    continue;
+                }
                 if (!outm) {   // statistics only: running sum of this chunk, no P, no O
                     float sq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -371,6 +454,48 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 fence_proxy_async_smem();
                 mbar_arrive(&p_full[quad]);
                 if (lane == 0) TRC(warp + 8, ti, 23);
+            }
+            if (hand) {
+                // ---- hat_alpha_R of the 4 columns: thread = key (its TMEM lane), D_i row / c_R ----
+                named_sync(1, 128);   // every column's c_R in shared memory
+                const int key = quad * 32 + lane;
+                const int u = gi;     // nch == 1
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+                for (int i = 0; i < 4; ++i) {
+                    mbar_wait(&o_done[i], u & 1);
+                    tc_fence_after();
+                    const float cr = reinterpret_cast<const float*>(smem + ColSmem::kOut + 16384)[i * 128 + key];
+                    const float inv = 1.f / fmaxf(cr, g.eps_div);
+                    const bool store = j0 + i < g.s2 && quad * 32 < g.nkeys;
+#pragma unroll 1
+                    for (int part = 0; part < 2; ++part) {
+                        float o[64];
+                        tmem_ld32(tmem + i * 128 + part * 64 + lane_off, o);
+                        tmem_ld32(tmem + i * 128 + part * 64 + 32 + lane_off, o + 32);
+                        if (!store) continue;
+                        uint8_t* stg = smem + ColSmem::kOut + quad * 4096;   // [32 keys][64 values], SW128
+                        if (lane == 0) bulk_wait_read<0>();
+                        __syncwarp();
+                        const uint32_t srow = smem_u32(stg) + lane * 128;
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc)
+                            st_shared_v4(srow + ((cc ^ (lane & 7)) << 4), pack_bf16(o[8 * cc] * inv, o[8 * cc + 1] * inv),
+                                         pack_bf16(o[8 * cc + 2] * inv, o[8 * cc + 3] * inv),
+                                         pack_bf16(o[8 * cc + 4] * inv, o[8 * cc + 5] * inv),
+                                         pack_bf16(o[8 * cc + 6] * inv, o[8 * cc + 7] * inv));
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {   // box rows past nkeys are clipped
+                            tma_store_4d(&P.tar_st, stg, part * 64, j0 + i, quad * 32, bh * g.gq + a);
+                            bulk_commit();
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(o_free);
+                named_sync(1, 128);   // c_R smem reused by the next group
+                continue;
             }
             if (!outm) {   // L statistics of row l of column j0 + quad (log2 units, x = S sl2 - c_L log2e)
                 if (j0 + quad < g.s2) {
