@@ -65,6 +65,20 @@ CONFIGS = {
                  "C4c N=32760 untiled aligned (fh,w) = (630,52)"),
     "n32k_mis": (1, 12, 21, 21, 30, 52, 128, "mis", "bf16",
                  "C4d N=32760 untiled misaligned raw (b1,b2) = (1260,26)"),
+    "n32k_f": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("f",)), "bf16",
+               "C4e N=32760 untiled aligned (f, hw) = (21,1560) (long tile rows: online-softmax row stage)"),
+    "sf720": (1, 12, 3, 3, 45, 80, 128, (1, 45, 80), "bf16",
+              "720p Self-Forcing chunk: B=1 H=12, 3 frames x (45,80), (h,w)-tiled (PAPER.md:866 shapes)"),
+    "sf720_3hw": (1, 12, 3, 3, 45, 80, 128, (3, 45, 80), "bf16",
+                  "720p Self-Forcing chunk, (3h,w) plan"),
+    "kv21_720": (1, 12, 21, 3, 45, 80, 128, (1, 45, 80), "bf16",
+                 "720p chunked-KV rollout: 3 query frames vs 21 KV frames of (45,80), (h,w)-tiled (paper s=0.97)"),
+    "kv21_720_3hw": (1, 12, 21, 3, 45, 80, 128, (3, 45, 80), "bf16",
+                     "720p chunked-KV rollout, (3h,w)-tiled (paper s=0.98)"),
+    "n75k_720": (1, 12, 21, 21, 45, 80, 128, (1, 45, 80), "bf16",
+                 "Wan 720p layer: N=75600 (21,45,80), (h,w)-tiled (PAPER.md:837, s=0.97)"),
+    "n75k_720_3hw": (1, 12, 21, 21, 45, 80, 128, (3, 45, 80), "bf16",
+                     "Wan 720p layer: N=75600 (21,45,80), (3h,w)-tiled (PAPER.md:837, s=0.98)"),
     "wan": (8, 12, 21, 21, 30, 52, 128, (1, 30, 52), "bf16",
             "C5 Wan-1.3B-shaped attention stack: 30 layers x B=8 H=12 N=32760 (h,w)-tiled (s=0.95), "
             "96 (b,h) units head-sharded over the ranks"),
@@ -81,8 +95,12 @@ def job_config(name, world, iterations):
     """The ``config`` dict both arms print (identical, so the driver can match them)."""
     B, H, fkv, fq, h, w, d, nb, dt, desc = CONFIGS[name]
     strong = name in STACKS
-    plan = {None: "untiled (fh,w)", "mis": "raw (1260,26)"}.get(nb, None) if not isinstance(nb, tuple) \
-        else f"neighborhoods {nb[0]}x{nb[1]}x{nb[2]}"
+    if isinstance(nb, tuple) and nb[0] == "aligned":
+        plan = f"aligned ({''.join(nb[1])}, rest)"
+    elif isinstance(nb, tuple):
+        plan = f"neighborhoods {nb[0]}x{nb[1]}x{nb[2]}"
+    else:
+        plan = {None: "untiled (fh,w)", "mis": "raw (1260,26)"}.get(nb)
     return {"workload": desc, "config": name, "B_per_layer": B, "H": H, "frames_q": fq, "frames_kv": fkv,
             "h": h, "w": w, "d": d, "plan": plan, "iterations": iterations,
             "layers_per_step": STACKS.get(name, world),
@@ -114,6 +132,9 @@ def workload(name, iterations):
         low = pk.lower_square(plan)
     elif nb == "mis":
         plan = pk.config_from_sizes(shape, 1260, 26)
+        low = pk.lower_square(plan)
+    elif nb[0] == "aligned":
+        plan = pk.aligned_config(shape, nb[1])
         low = pk.lower_square(plan)
     else:
         plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
@@ -272,8 +293,8 @@ def _cpu_unit(i):
         import monarchbench as mb
 
         shape = mb.VideoShape(wl["fkv"], wl["h"], wl["w"])
-        if wl["nb"] is None:
-            cfg = mb.aligned_config(shape, ("f", "h"))
+        if wl["nb"] is None or wl["nb"][0] == "aligned":
+            cfg = mb.aligned_config(shape, ("f", "h") if wl["nb"] is None else wl["nb"][1])
             fac, _ = mb.solve(mb.AttentionProblem(q, k, v, shape), cfg, mb.SolverConfig(iterations=T))
         elif wl["nb"] == "mis":
             cfg = mb.config_from_sizes(shape, 1260, 26)

@@ -91,6 +91,8 @@ struct TcParams {
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
     int l2hint;                           // W stores evict_last, last reads evict_first (MBX_L2HINT=0: off)
+    CUtensorMap tq128, tk128, tv128;      // flash row stage (s2 > 64): 128-row boxes of q / k / v
+    CUtensorMap tar_ld128;                // flash row stage, T >= 2: 128 hat_alpha_R rows of one key
     float* rfac;                          // optional R' export (fp32, factors.py:57-79 layout), last row stage
     float* lfac;                          // optional L' export, written by the alpha kernel in mode 1
 };
@@ -110,6 +112,7 @@ __device__ __forceinline__ void store_r_row(float* dst, const float* p, float in
 #include "mbx_tc_alpha.cuh"
 #include "mbx_tc_colw.cuh"
 #include "mbx_tc_rowp.cuh"
+#include "mbx_tc_rowf.cuh"
 
 __device__ __forceinline__ uint8_t* aligned_smem() {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -271,7 +274,7 @@ static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags
     if (flags & MBX_FLAG_FORCE_GENERIC) return "forced generic";
     if (flags & MBX_FLAG_NO_OUTPUT) return "factors without output";
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return "needs bf16 with d = dv = 128";
-    if (g.s2 > kMaxS2) return "s2 > 64";
+    if (factors && g.s2 > kMaxS2) return "factor export with s2 > 64";   // online row softmax (flash row stage)
     if (g.T > 1 && g.s1 > 128) return "T > 1 with s1 > 128";   // alpha_R hand-off: query rows l on the MMA N axis
     if (factors && g.s1 > 128) return "factor export with s1 > 128";   // L export shares the alpha_R kernel
     if (g.nf == 0 && (g.q_order || g.kv_order)) return "permuted plan without a closed form";
@@ -329,6 +332,8 @@ struct TcPlan {
     Geometry g;            // identity plans rewritten as a (1, s1, s2) neighborhood grid
     bool pair, wide;
     bool fused_hand;       // T >= 2 hand-off fused into the stacked column stage (mode 2)
+    bool flash;            // s2 > 64: online-softmax row stage
+    int grid_flash, smem_flash;
     int grid_pair, grid_row, grid_col, grid_wide, grid_alpha;
     int smem_row, smem_col, smem_pair, smem_wide, smem_alpha;
 };
@@ -354,9 +359,15 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
     P.l2hint = o.l2hint;
     P.rfac = r_factor;
     P.lfac = l_factor;
-    if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, g.s2) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, g.s2) ||
-        !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, g.s2) || !make_qcol_map(&P.tqc, q, g, nq) ||
+    const bool flash = g.s2 > kMaxS2;   // long tile rows: online-softmax row stage
+    const int rbox = flash ? kMaxS2 : g.s2;
+    if (!make_rows_map(&P.tq, q, B, g.heads, nq, g.qs, rbox) || !make_rows_map(&P.tk, k, B, g.heads, nk, g.ks, rbox) ||
+        !make_rows_map(&P.tv, v, B, g.heads, nk, g.vs, rbox) || !make_qcol_map(&P.tqc, q, g, nq) ||
         !make_outcol_map(&P.tout, out, g, nq))
+        return TC_FAIL("tensor map / argument check");
+    if (flash && (!make_rows_map(&P.tq128, q, B, g.heads, nq, g.qs, kFKC) ||
+                  !make_rows_map(&P.tk128, k, B, g.heads, nk, g.ks, kFKC) ||
+                  !make_rows_map(&P.tv128, v, B, g.heads, nk, g.vs, kFKC)))
         return TC_FAIL("tensor map / argument check");
     const int64_t ncols = (int64_t)g.bh * g.gq * g.s2;
     const int64_t rows = ncols * g.nkeys;
@@ -393,19 +404,16 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
         cuuint32_t box[4] = {64, (cuuint32_t)kKC, 1, 1};          // column stage: contiguous 12 KB
         if (!encode(&P.tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
             return TC_FAIL("tensor map / argument check");
-        // row stage: one key, the columns j of one epilogue warp (rows 0..31 and 32..s2-1)
-        cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 32 ? g.s2 : 32)};
-        if (!encode(&P.tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
-            return TC_FAIL("tensor map / argument check");
-        cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
-        if (!encode(&P.tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b, CU_TENSOR_MAP_SWIZZLE_128B))
-            return TC_FAIL("tensor map / argument check");
-        cuuint32_t sbox16[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 16 ? g.s2 : 16)};
-        cuuint32_t sbox16r[4] = {64, 1, 1, (cuuint32_t)(g.s2 % 16 ? g.s2 % 16 : 16)};
-        if (!encode(&P.tws16, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox16, CU_TENSOR_MAP_SWIZZLE_128B) ||
-            !encode(&P.tws16r, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox16r,
-                    CU_TENSOR_MAP_SWIZZLE_128B))
-            return TC_FAIL("tensor map / argument check");
+        if (!flash) {
+            // classic row stage: one key, the columns j of one epilogue warp (rows 0..31 and 32..s2-1)
+            cuuint32_t sbox[4] = {64, 1, 1, (cuuint32_t)(g.s2 < 32 ? g.s2 : 32)};
+            if (!encode(&P.tws, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
+                return TC_FAIL("tensor map / argument check");
+            cuuint32_t sbox_b[4] = {64, 1, 1, (cuuint32_t)(g.s2 > 32 ? g.s2 - 32 : 1)};
+            if (!encode(&P.tws_b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, Wp, dims, strides, sbox_b,
+                        CU_TENSOR_MAP_SWIZZLE_128B))
+                return TC_FAIL("tensor map / argument check");
+        }
         cuuint64_t cdims[2] = {(cuuint64_t)ckey_stride(g), (cuuint64_t)ncols};
         cuuint64_t cstrides[1] = {(cuuint64_t)ckey_stride(g) * 4};
         cuuint32_t cbox[2] = {(cuuint32_t)kKC, 1};
@@ -427,11 +435,14 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
             cuuint64_t adims[4] = {128, (cuuint64_t)g.s2, (cuuint64_t)g.nkeys, (cuuint64_t)g.bh * g.gq};
             cuuint64_t astr[3] = {256, (cuuint64_t)g.s2 * 256, (cuuint64_t)g.s2 * 256 * g.nkeys};
             cuuint32_t abox_st[4] = {64, 1, 32, 1};
-            cuuint32_t abox_ld[4] = {64, (cuuint32_t)g.s2, 1, 1};
+            cuuint32_t abox_ld[4] = {64, (cuuint32_t)rbox, 1, 1};
+            cuuint32_t abox_ld128[4] = {64, (cuuint32_t)kFKC, 1, 1};
             if (!encode(&P.tar_st, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_st,
                         CU_TENSOR_MAP_SWIZZLE_128B) ||
                 !encode(&P.tar_ld, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_ld,
-                        CU_TENSOR_MAP_SWIZZLE_128B))
+                        CU_TENSOR_MAP_SWIZZLE_128B) ||
+                (flash && !encode(&P.tar_ld128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, AR, adims, astr, abox_ld128,
+                                  CU_TENSOR_MAP_SWIZZLE_128B)))
                 return TC_FAIL("tensor map / argument check");
         }
     }
@@ -439,6 +450,12 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
     const int sms = num_sms(dev);
     T->g = g;
     T->wide = wide;
+    T->flash = flash;
+    T->smem_flash = RowFSmem::kTotal + 1024;
+    {
+        const int64_t ftasks = (int64_t)g.bh * g.gq * g.s1 * ((g.s2 + kFKC - 1) / kFKC) * g.gk;
+        T->grid_flash = ftasks < sms ? (int)ftasks : sms;
+    }
     T->fused_hand = !wide && g.T > 1 && g.nkeys <= kKC && o.fusedhand != 0;
     T->smem_row = RowSmem::kTotal + 1024;
     T->smem_col = ColSmem::kTotal + 1024;
@@ -529,7 +546,7 @@ static cudaError_t ensure_attributes(int dev) {
     const struct { const void* fn; int smem; } k[] = {
         {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage, ColSmem::kTotal + 1024},
         {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
-        {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}};
+        {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}, {(const void*)tc_row_flash, RowFSmem::kTotal + 1024}};
     for (auto& x : k)
         if ((e = cudaFuncSetAttribute(x.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x.smem)) != cudaSuccess)
             return e;
@@ -599,7 +616,12 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
         int last = t == g.T - 1, amode = t > 0;
         Pt.rfac = !r_factor ? nullptr : all_iters ? r_factor + t * rslice : last ? r_factor : nullptr;
         Pt.lfac = !l_factor ? nullptr : all_iters ? l_factor + t * lslice : last ? l_factor : nullptr;
-        if (T.pair) {
+        if (T.flash) {
+            ProfScope p("tc_row_flash", stream);
+            void* args[] = {(void*)&Pt, (void*)&g, (void*)&amode, (void*)&last};
+            if ((e = launch((const void*)tc_row_flash, T.grid_flash, kFThreads, T.smem_flash, args)) != cudaSuccess)
+                return e;
+        } else if (T.pair) {
             ProfScope p("tc_row_pair", stream);
             void* args[] = {(void*)&Pt, (void*)&g, (void*)&amode, (void*)&last};
             if ((e = launch((const void*)tc_row_pair, T.grid_pair, kPairThreads, T.smem_pair, args)) != cudaSuccess)

@@ -148,3 +148,40 @@ def test_solve_tiled_bf16_reaches_tensor_cores(cuda):
     assert orc.rel_l2(fac.r_blocks, R) < BF16_TOL
     out = pk.attention_output(fac, v.float().numpy())
     assert orc.rel_l2(out, ref) < BF16_TOL
+
+
+# Long tile rows (s2 > 64) -> the online-softmax row stage (tc_row_flash): the paper's 720p
+# latent grid (h, w) = (45, 80) and the aligned (f, hw) configuration.
+FLASH = [
+    ("sf720_hw", (3, 45, 80), ("nb", (1, 45, 80)), None, 1, 2),
+    ("sf720_hw_T2", (3, 45, 80), ("nb", (1, 45, 80)), None, 2, 1),
+    ("sf720_3hw", (3, 45, 80), ("nb", (3, 45, 80)), None, 1, 1),
+    ("kv9_720_hw", (9, 45, 80), ("nb", (1, 45, 80)), 3, 1, 1),
+    ("n32k_f", (21, 30, 52), ("aligned", ("f",)), None, 1, 1),
+    ("n32k_f_T2", (21, 30, 52), ("aligned", ("f",)), None, 2, 1),
+    ("raw_b2_200", (4, 10, 60), ("raw", 12, 200), None, 1, 2),
+    ("raw_b2_100_T3", (2, 10, 30), ("raw", 6, 100), None, 3, 1),
+]
+
+
+def _plan_kind(fhw, kind):
+    shape = pk.VideoShape(*fhw)
+    if kind[0] == "nb":
+        return pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), kind[1])
+    if kind[0] == "aligned":
+        return pk.aligned_config(shape, kind[1])
+    return pk.config_from_sizes(shape, kind[1], kind[2])
+
+
+@pytest.mark.parametrize("name,fhw,kind,q_frames,T,H", FLASH, ids=[c[0] for c in FLASH])
+def test_long_tile_rows_flash_row_stage(cuda, name, fhw, kind, q_frames, T, H):
+    plan = _plan_kind(fhw, kind)
+    low = pk.lower_chunked(plan, q_frames) if q_frames else pk.lower_square(plan)
+    assert low.s2 > 64
+    q, k, v = _inputs(zlib.crc32(name.encode()) % 1000, H, low.n_q, low.n_kv, cuda)
+    assert ops.selected_path(q, k, v, low, T) == "tcgen05", name
+    out = ops.forward(q, k, v, low, T)
+    for h in range(H):
+        _, _, ref = _oracle(q, k, v, low, T, 0, h)
+        err = orc.rel_l2(out[0, h].float().cpu().numpy(), ref)
+        assert err < BF16_TOL, (name, h, err)
