@@ -194,7 +194,13 @@ int mbx_profile_collect_ex(float* start_ms, float* ms, const char** names, int m
  * default 1), "MBX_L2HINT" (L2 residency hints, 1), "MBX_PAIR" (row-stage
  * variant, -1 auto / 0 classic / 1 half-packed), "MBX_WIDE" (wide column stage
  * for s1 <= 32, 0), "MBX_SPLIT" (concurrent halves, -1 auto / 0 / 1),
- * "MBX_DBG" (timing bits, results wrong), "MBX_VERBOSE".  Returns the previous
+ * "MBX_DBG" (timing bits, results wrong), "MBX_VERBOSE", "MBX_WAVE" ((b,h)
+ * slices per wave of the tensor-core path, -1 automatic, 0 one wave) and
+ * "MBX_WS_CAP_MB" (automatic waves keep the workspace under this many MiB,
+ * default 2048; waves run in sequence on `stream` and reuse one workspace
+ * region -- the mini-sequence chunking of the paper).  Options that change
+ * the workspace size must not change between mbx_workspace_bytes and
+ * mbx_forward.  Returns the previous
  * value, or -1000 for an unknown name.  Not for use while another thread is
  * enqueueing forwards.
  */

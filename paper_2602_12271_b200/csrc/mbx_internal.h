@@ -82,6 +82,8 @@ struct Options {
     int split = -1;     // concurrent halves: 0 off, 1 on
     int verbose = 0;    // print why a problem leaves the tcgen05 path / setup failures
     int fusedhand = 1;  // T >= 2: alpha_R hand-off inside the column stage when a column is one key chunk
+    int wave = -1;      // (b, h) slices per wave of the tensor-core path: -1 from the cap, 0 one wave
+    int ws_cap_mb = 2048;   // automatic waves keep the tensor-core workspace under this many MiB
     unsigned version = 0;   // bumped on every change (keys the launch-parameter cache)
 };
 const Options& options();

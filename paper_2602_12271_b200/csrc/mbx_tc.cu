@@ -126,12 +126,16 @@ tc_row_stage(const __grid_constant__ TcParams P, Geometry g, int amode, int want
     SPAN_AT(0, 1);
 }
 
+template <int mode>
 __global__ void __launch_bounds__(kColThreads, 1)
-tc_column_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
+tc_column_stage(const __grid_constant__ TcParams P, Geometry g) {
     SPAN_AT(1, 0);
-    col_role(aligned_smem(), P, g, blockIdx.x, gridDim.x, mode);
+    col_role<mode>(aligned_smem(), P, g, blockIdx.x, gridDim.x);
     SPAN_AT(1, 1);
 }
+template __global__ void tc_column_stage<0>(const __grid_constant__ TcParams, Geometry);
+template __global__ void tc_column_stage<1>(const __grid_constant__ TcParams, Geometry);
+template __global__ void tc_column_stage<2>(const __grid_constant__ TcParams, Geometry);
 
 // ===================================================================== host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -193,6 +197,9 @@ bool make_qcol_map(CUtensorMap* m, const void* base, const Geometry& g, int nq) 
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+constexpr size_t kPairKvBytes = (size_t)48 << 20;   // K + V of a launch the half-packed stage re-reads from L2
+constexpr long long kWavePairTasks = 2000;           // per-head pair tasks that make L2-sized waves pay
+
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int num_sms(int dev) {   // per device (mixed-GPU hosts)
@@ -244,6 +251,8 @@ static void init_options() {
     g_opts.split = env("MBX_SPLIT", -1);
     g_opts.verbose = env("MBX_VERBOSE", 0);
     g_opts.fusedhand = env("MBX_FUSEDHAND", 1);
+    g_opts.wave = env("MBX_WAVE", -1);
+    g_opts.ws_cap_mb = env("MBX_WS_CAP_MB", 2048);
 }
 
 const Options& options() {
@@ -258,7 +267,8 @@ int set_option(const char* name, int value) {
     struct { const char* n; int* p; } tab[] = {
         {"MBX_PDL", &g_opts.pdl}, {"MBX_L2HINT", &g_opts.l2hint}, {"MBX_DBG", &g_opts.dbg},
         {"MBX_PAIR", &g_opts.pair}, {"MBX_WIDE", &g_opts.wide}, {"MBX_SPLIT", &g_opts.split},
-        {"MBX_VERBOSE", &g_opts.verbose}, {"MBX_FUSEDHAND", &g_opts.fusedhand}};
+        {"MBX_VERBOSE", &g_opts.verbose}, {"MBX_FUSEDHAND", &g_opts.fusedhand},
+        {"MBX_WAVE", &g_opts.wave}, {"MBX_WS_CAP_MB", &g_opts.ws_cap_mb}};
     for (auto& t : tab)
         if (strcmp(t.n, name) == 0) {
             const int prev = *t.p;
@@ -471,7 +481,7 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
     // query tiles leave M=128 lanes idle (odd G_q); for G_q > 1 a K/V row then serves halves
     // of two items, so it is re-read once more -- cheap only while K and V sit in L2.
     const size_t kv_bytes = (size_t)g.bh * g.gk * g.s1 * g.s2 * (size_t)(g.d + g.dv) * 2;
-    T->pair = o.pair >= 0 ? o.pair == 1 : g.gq == 1 || (g.gq % 2 == 1 && kv_bytes <= ((size_t)48 << 20));
+    T->pair = o.pair >= 0 ? o.pair == 1 : g.gq == 1 || (g.gq % 2 == 1 && kv_bytes <= kPairKvBytes);
     const int64_t pair_tasks = (int64_t)g.bh * ((g.gq * g.s1 + 1) / 2) * g.gk;
     T->grid_pair = pair_tasks < sms ? (int)pair_tasks : sms;
     const int64_t ngroups = (int64_t)g.bh * g.gq * ((g.s2 + 3) / 4);
@@ -544,7 +554,8 @@ static cudaError_t ensure_attributes(int dev) {
     if (done[dev]) return cudaSuccess;
     cudaError_t e;
     const struct { const void* fn; int smem; } k[] = {
-        {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage, ColSmem::kTotal + 1024},
+        {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage<0>, ColSmem::kTotal + 1024},
+        {(const void*)tc_column_stage<1>, ColSmem::kTotal + 1024}, {(const void*)tc_column_stage<2>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
         {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}, {(const void*)tc_row_flash, RowFSmem::kTotal + 1024}};
     for (auto& x : k)
@@ -556,7 +567,7 @@ static cudaError_t ensure_attributes(int dev) {
 
 static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, const void* k, const void* v,
                                   void* out, float* l_factor, float* r_factor, void* workspace, int dev,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, bool pdl_first = false) {
     cudaError_t e = ensure_attributes(dev);
     if (e != cudaSuccess) return e;
     TcPlan T;
@@ -570,7 +581,7 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
     // while the previous stage drains and wait (griddepcontrol.wait) before touching
     // the workspace.  The first launch is ordinary, so it never overlaps the previous
     // forward's readers of the workspace.
-    int nlaunch = 0;
+    int nlaunch = pdl_first ? 1 : 0;
     auto launch = [&](const void* fn, int grid, int threads, int smem, void** args) -> cudaError_t {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
@@ -595,8 +606,10 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
             return launch((const void*)tc_column_wide, T.grid_wide, kWideThreads, T.smem_wide, args);
         }
         ProfScope p("tc_column_stage", stream);
-        void* args[] = {(void*)&Pc, (void*)&g, (void*)&mode};
-        return launch((const void*)tc_column_stage, T.grid_col, kColThreads, T.smem_col, args);
+        void* args[] = {(void*)&Pc, (void*)&g};
+        const void* fn = mode == 0 ? (const void*)tc_column_stage<0>
+                         : mode == 1 ? (const void*)tc_column_stage<1> : (const void*)tc_column_stage<2>;
+        return launch(fn, T.grid_col, kColThreads, T.smem_col, args);
     };
     auto alpha = [&](int amode, TcParams& Pc) -> cudaError_t {
         ProfScope p(amode ? "tc_alpha_l_export" : "tc_alpha_r_stage", stream);
@@ -670,9 +683,89 @@ static Geometry half_heads(const Geometry& g) {   // B = 1: first half of the he
     return h;
 }
 
+// Waves: the (b, h) slices of one launch sequence run as consecutive waves of nb batches x nh
+// heads (nh < heads only with nb = 1) that reuse one workspace region, so the workspace is
+// capped (the paper's mini-sequence chunking) and, for small waves, the W
+// exchange of a wave can stay L2-resident between its row and column stages.  The wave
+// size is MBX_WAVE (b, h) slices per wave when set, else the largest that keeps the
+// workspace under MBX_WS_CAP_MB.  Factor export runs as one wave (factor slices are laid
+// out for the whole problem).
+struct WavePlan {
+    int nb, nh;
+};
+static Geometry wave_geom(const Geometry& g, int nb, int nh) {
+    Geometry w = g;
+    w.heads = nh;
+    w.bh = nb * nh;
+    return w;
+}
+static WavePlan tc_wave_plan(const Geometry& g, int flags) {
+    const int B = g.bh / g.heads, H = g.heads;
+    WavePlan w{B, H};
+    if (flags & MBX_FLAG_FACTORS) return w;
+    const Options& o = options();
+    long long per = o.wave;
+    if (per == 0) return w;
+    if (per < 0) {
+        const size_t cap = (size_t)(o.ws_cap_mb > 0 ? o.ws_cap_mb : 1) << 20;
+        const size_t one = tc_layout(wave_geom(g, 1, 1)).total;
+        per = (long long)(cap / (one ? one : 1));
+        // Long problems with an odd number of query tiles: one-head waves, whose K / V sit in
+        // L2, run the half-packed row stage (a K/V row serves halves of two items from L2) --
+        // N=32k (h,w) 2.03 -> 1.72 ms (waves of 3 / 2 heads: 1.96 / 1.85), (3h,w) 0.88 -> 0.85 ms;
+        // only when one head still gives every SM dozens of row tasks (KV21 (h,w), 945 tasks
+        // per head, loses: 0.276 -> 0.376 ms).
+        const size_t kv_head = (size_t)g.gk * g.s1 * g.s2 * (size_t)(g.d + g.dv) * 2;
+        const long long pair_tasks_head = (long long)((g.gq * g.s1 + 1) / 2) * g.gk;
+        if (o.pair < 0 && g.gq > 1 && g.gq % 2 == 1 && g.s2 <= kMaxS2 && kv_head <= kPairKvBytes &&
+            (size_t)g.bh * kv_head > kPairKvBytes && pair_tasks_head >= kWavePairTasks)
+            per = 1;
+        if (per < 1) per = 1;
+    }
+    if (per >= g.bh) return w;
+    if (per >= H) {
+        w.nb = (int)(per / H);
+    } else {
+        w.nb = 1;
+        w.nh = (int)per;
+    }
+    return w;
+}
+static size_t tc_wave_bytes(const Geometry& g, int flags) {
+    const WavePlan w = tc_wave_plan(g, flags);
+    return tc_layout(wave_geom(g, w.nb, w.nh)).total;
+}
+
 size_t tc_workspace_bytes(const Geometry& g, int flags) {
-    if (tc_split(g, flags)) return 2 * align256(tc_layout(half_heads(g)).total);
-    return tc_layout(g).total;
+    if (tc_split(g, flags)) return 2 * align256(tc_wave_bytes(half_heads(g), flags));
+    return tc_wave_bytes(g, flags);
+}
+
+// One launch sequence per wave, in (batch, head) order on `stream`; later waves use PDL
+// (every stage waits for its predecessor before it touches the shared workspace).
+static cudaError_t tc_forward_waves(const Geometry& g, int flags, const void* q, const void* k, const void* v,
+                                    void* out, float* l_factor, float* r_factor, void* workspace, int dev,
+                                    cudaStream_t stream) {
+    const WavePlan w = tc_wave_plan(g, flags);
+    const int B = g.bh / g.heads, H = g.heads;
+    if (w.nb == B && w.nh == H)
+        return tc_forward_one(g, flags, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
+    auto at = [](const void* p, const int64_t* st, int b, int h) {
+        return const_cast<char*>(reinterpret_cast<const char*>(p)) + ((size_t)b * st[0] + (size_t)h * st[1]) * 2;
+    };
+    bool first = true;
+    for (int b0 = 0; b0 < B; b0 += w.nb) {
+        const int nb = B - b0 < w.nb ? B - b0 : w.nb;
+        for (int h0 = 0; h0 < H; h0 += w.nh) {
+            const int nh = H - h0 < w.nh ? H - h0 : w.nh;
+            const Geometry gw = wave_geom(g, nb, nh);
+            cudaError_t e = tc_forward_one(gw, flags, at(q, g.qs, b0, h0), at(k, g.ks, b0, h0), at(v, g.vs, b0, h0),
+                                           at(out, g.os, b0, h0), nullptr, nullptr, workspace, dev, stream, !first);
+            if (e != cudaSuccess) return e;
+            first = false;
+        }
+    }
+    return cudaSuccess;
 }
 
 // Side stream + fork/join events of one (device, caller stream); created all-or-nothing.
@@ -738,19 +831,18 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
         ss = side_for(dev, stream, cs == cudaStreamCaptureStatusNone);
     }
     if (!ss) {
-        Geometry g1 = g;
-        return tc_forward_one(g1, flags, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
+        return tc_forward_waves(g, flags, q, k, v, out, l_factor, r_factor, workspace, dev, stream);
     }
     const Geometry h = half_heads(g);
-    const size_t wsh = align256(tc_layout(h).total);
+    const size_t wsh = align256(tc_wave_bytes(h, flags));
     auto at = [&](const void* p, const int64_t* st) {   // start of the second half (bf16 elements)
         const size_t off = g.bh == g.heads ? (size_t)h.heads * (size_t)st[1] : (size_t)(h.bh / h.heads) * (size_t)st[0];
         return reinterpret_cast<const char*>(p) + off * 2;
     };
     if ((e = cudaEventRecord(ss->fork, stream)) != cudaSuccess || (e = cudaStreamWaitEvent(ss->side, ss->fork, 0)) != cudaSuccess)
         return e;
-    cudaError_t e1 = tc_forward_one(h, flags, q, k, v, out, nullptr, nullptr, workspace, dev, stream);
-    cudaError_t e2 = tc_forward_one(h, flags, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
+    cudaError_t e1 = tc_forward_waves(h, flags, q, k, v, out, nullptr, nullptr, workspace, dev, stream);
+    cudaError_t e2 = tc_forward_waves(h, flags, at(q, g.qs), at(k, g.ks), at(v, g.vs), const_cast<char*>(at(out, g.os)),
                                     nullptr, nullptr, reinterpret_cast<char*>(workspace) + wsh, dev, ss->side);
     // the join is recorded even if a half failed, so the side stream never dangles outside a capture
     if ((e = cudaEventRecord(ss->join, ss->side)) != cudaSuccess || (e = cudaStreamWaitEvent(stream, ss->join, 0)) != cudaSuccess)

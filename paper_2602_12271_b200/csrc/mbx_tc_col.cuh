@@ -39,10 +39,10 @@ struct ColSmem {
 // runs into TMEM (D_i at columns 128 i, over the consumed S regions); c_R = sum_l L is a
 // warp transpose-reduce of the fp32 L row; the epilogue writes hat_alpha_R = alpha_R /
 // max(c_R, eps) (bf16) for the next row stage -- no statistics pass, no alpha_R stage.
-__device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride,
-                                         int mode = 0) {
-    const bool outm = mode == 0;
-    const bool hand = mode == 2;
+template <int mode>   // compile-time: each mode gets its own register allocation
+__device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride) {
+    constexpr bool outm = mode == 0;
+    constexpr bool hand = mode == 2;
     const CUtensorMap& tm_w = P.tw;
     const CUtensorMap& tm_c = P.tc;
     const CUtensorMap& tm_qc = P.tqc;
