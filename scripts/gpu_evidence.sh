@@ -8,12 +8,17 @@ timeout 900 python bench.py > gpurun_out/ev/bench_default.json 2> gpurun_out/ev/
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ev/bench_reference.json 2> gpurun_out/ev/bench_reference.err
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
     bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > gpurun_out/ev/bench_torchrun1.json 2> gpurun_out/ev/bench_torchrun1.err
+# two ranks sharing the box's one GPU (self-launched under torch.distributed.run; gloo barrier / max)
+timeout 600 python bench.py --gpus 2 --steps 10 --warmup 3 --no-cpu --no-backward > gpurun_out/ev/bench_gpus2.json 2> gpurun_out/ev/bench_gpus2.err
+timeout 900 python bench.py --gpus 2 --config wan --steps 2 --warmup 3 --no-cpu --no-backward > gpurun_out/ev/bench_wan_gpus2.json 2> gpurun_out/ev/bench_wan_gpus2.err
 : > gpurun_out/ev/sweep.jsonl
 for a in "--config sf" "--config sf --iters 2" "--config sf --iters 3" "--config sf3hw" \
          "--config kv21" "--config kv21 --iters 2" "--config kv21 --iters 3" "--config kv21_3hw" \
          "--config kv21_3hw --iters 2" "--config kv21_3hw --iters 3" \
-         "--config n32k" "--config n32k_3hw" "--config n32k_fhw" "--config n32k_mis" "--config c1"; do
-  timeout 600 python bench.py --steps 10 --warmup 3 $a --no-cpu 2>/dev/null | tail -1 | python -c "
+         "--config n32k" "--config n32k_3hw" "--config n32k_fhw" "--config n32k_mis" "--config n32k_f" "--config c1" \
+         "--config sf720" "--config sf720_3hw" "--config kv21_720_3hw" "--config n75k_720_3hw" "--config wan --steps 2" \
+         "--config wan_3hw --steps 2"; do
+  timeout 900 python bench.py --steps 10 --warmup 3 $a --no-cpu --no-backward 2>/dev/null | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); d['args']='$a'; print(json.dumps(d))" >> gpurun_out/ev/sweep.jsonl
 done
