@@ -136,9 +136,15 @@ def profile_collect_ex(max_entries: int = 4096) -> list[tuple[str, float, float]
     return [(names[i].decode(), float(st[i]), float(ms[i])) for i in range(min(n, max_entries))]
 
 
+# bumped on every option change: options such as MBX_WAVE / MBX_WS_CAP_MB change the
+# workspace size, so host-side caches of mbx_workspace_bytes key on it
+OPTIONS_VERSION = [0]
+
+
 def set_option(name: str, value: int) -> int:
     """Process-wide diagnostic option (mbx_set_option); returns the previous value."""
     prev = load().mbx_set_option(name.encode(), int(value))
     if prev == -1000:
         raise KeyError(name)
+    OPTIONS_VERSION[0] += 1
     return prev

@@ -131,7 +131,7 @@ _WS: dict = {}
 
 def _prepared(q, k, v, out, low, iterations, scale, eps_div, eps_log, flags):
     key = (q.shape, q.stride(), k.shape, k.stride(), v.shape, v.stride(), out.shape, out.stride(),
-           q.dtype, q.device, id(low), iterations, scale, eps_div, eps_log, flags)
+           q.dtype, q.device, id(low), iterations, scale, eps_div, eps_log, flags, _lib.OPTIONS_VERSION[0])
     hit = _PREP.get(key)
     if hit is not None and hit[0] is low:
         return hit[1], hit[2]
