@@ -720,6 +720,11 @@ static WavePlan tc_wave_plan(const Geometry& g, int flags) {
         if (o.pair < 0 && g.gq > 1 && g.gq % 2 == 1 && g.s2 <= kMaxS2 && kv_head <= kPairKvBytes &&
             (size_t)g.bh * kv_head > kPairKvBytes && pair_tasks_head >= kWavePairTasks)
             per = 1;
+        // Long tile rows (online-softmax row stage): one-head waves keep a head's K / V in L2
+        // while its row tasks stream them -- Wan 720p layer (h,w) 8.67 -> 7.90 ms, (3h,w)
+        // 3.74 -> 3.50 ms; KV21 720p (945 tasks per head) and (f,hw) N=32k (273) lose.
+        const long long flash_tasks_head = (long long)g.gq * g.s1 * ((g.s2 + kFKC - 1) / kFKC) * g.gk;
+        if (o.pair < 0 && g.s2 > kMaxS2 && g.bh > 1 && flash_tasks_head >= kWavePairTasks) per = 1;
         if (per < 1) per = 1;
     }
     if (per >= g.bh) return w;
