@@ -132,8 +132,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             // which the softmax threads finish before arriving on p_full(it))
             mbar_wait(&p_full[b], (it >> 1) & 1);
             tc_fence_after();
-            if (leader && lexp) {   // L export: no alpha_R product
-                mma_commit(&o_full[b]);
+            if (leader && lexp) {   // L export: no alpha_R product (and no o_full: nobody drains D2)
                 mma_commit(&ld_empty[b]);
             } else if (leader) {
                 for (int kk = 0; kk < s1p / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
