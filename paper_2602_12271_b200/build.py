@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False, varia
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp_lib = lib + ".tmp"
-    subprocess.run([nvcc(), "-shared", "-o", tmp_lib] + objs + ARCH + ["-lcuda"], check=True)
+    subprocess.run([nvcc(), "-shared", "-o", tmp_lib] + objs + ARCH + ["-lcuda", "-ldl"], check=True)
     os.replace(tmp_lib, lib)
     return lib
 

@@ -19,7 +19,10 @@
 // oracle is torch autograd of oracle/monarch_torch.py (tests/test_backward_gpu.py).
 #include "mbx_internal.h"
 
+#include <cublas_v2.h>
+#include <dlfcn.h>
 #include <math.h>
+#include <mutex>
 
 namespace mbx {
 namespace {
@@ -267,6 +270,115 @@ __global__ void scatter_tiles(const Geometry g, const float* __restrict__ src, c
     }
 }
 
+// ------------------------------------------------------------------ cuBLAS (bf16 I/O)
+// For bf16 I/O (the 2e-2 tolerance) the contractions run as TF32 tensor-core batched
+// GEMMs through cuBLAS (plain library GEMMs: per-batch pointers from a fill kernel, the
+// two-level reduction index split into K1 accumulating calls when it is not contiguous).
+// libcublas is opened at first use (dlopen of the soname PyTorch already loaded, else the
+// CUDA toolkit's), so the forward library has no link-time dependency on it.  fp32 I/O
+// (the 1e-4 parity mode) keeps the fp32 SIMT GEMM above.
+typedef cublasStatus_t (*CreateFn)(cublasHandle_t*);
+typedef cublasStatus_t (*SetStreamFn)(cublasHandle_t, cudaStream_t);
+typedef cublasStatus_t (*GemmBatchedExFn)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                                          const void*, const void* const[], cudaDataType, int, const void* const[],
+                                          cudaDataType, int, const void*, void* const[], cudaDataType, int, int,
+                                          cublasComputeType_t, cublasGemmAlgo_t);
+struct Cublas {
+    CreateFn create = nullptr;
+    SetStreamFn set_stream = nullptr;
+    GemmBatchedExFn gemm = nullptr;
+    bool ok = false;
+};
+const Cublas& cublas() {
+    static Cublas c;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libcublas.so.12", "/usr/local/cuda/lib64/libcublas.so.12", "libcublas.so"};
+        void* h = nullptr;
+        for (const char* n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL)) != nullptr) break;
+        if (!h) return;
+        c.create = reinterpret_cast<CreateFn>(dlsym(h, "cublasCreate_v2"));
+        c.set_stream = reinterpret_cast<SetStreamFn>(dlsym(h, "cublasSetStream_v2"));
+        c.gemm = reinterpret_cast<GemmBatchedExFn>(dlsym(h, "cublasGemmBatchedEx"));
+        c.ok = c.create && c.set_stream && c.gemm;
+    });
+    return c;
+}
+// one handle per (thread, device): cuBLAS handles are not for concurrent use across threads
+cublasHandle_t cublas_handle() {
+    thread_local cublasHandle_t h[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!h[dev] && cublas().ok && cublas().create(&h[dev]) != CUBLAS_STATUS_SUCCESS) h[dev] = nullptr;
+    return h[dev];
+}
+
+// pointer arrays of one batched call: batch b = (b0, b1, b2, b3) row-major over nb
+__global__ void fill_ptrs(Gemm G, int64_t a_off, int64_t b_off, const float** pa, const float** pb, float** pc,
+                          int64_t n) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t x = i;
+    int bi[4];
+    bi[3] = (int)(x % G.nb[3]); x /= G.nb[3];
+    bi[2] = (int)(x % G.nb[2]); x /= G.nb[2];
+    bi[1] = (int)(x % G.nb[1]); x /= G.nb[1];
+    bi[0] = (int)x;
+    int64_t oa = a_off, ob = b_off, oc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        oa += bi[k] * G.A.b[k];
+        ob += bi[k] * G.B.b[k];
+        oc += bi[k] * G.C.b[k];
+    }
+    pa[i] = G.A.p + oa;
+    pb[i] = G.B.p + ob;
+    pc[i] = const_cast<float*>(G.C.p) + oc;
+}
+
+// C (row-major M x N, ld C.s0) = alpha A B^T (+ C): cuBLAS column-major C^T = op(B) op(A^T)
+bool gemm_tf32(const Gemm& G, void** ptrs, int64_t max_batches, cudaStream_t st) {
+    const Cublas& cb = cublas();
+    cublasHandle_t h = cublas_handle();
+    if (!cb.ok || !h || G.C.s1 != 1) return false;
+    const int64_t batches = (int64_t)G.nb[0] * G.nb[1] * G.nb[2] * G.nb[3];
+    if (batches > max_batches || batches > INT32_MAX) return false;
+    // K index: flattened when k1 and k2 form one stride (or one of them is trivial), else K1 calls
+    auto kstride = [&](const Operand& o, int64_t& sk, bool& flat) {
+        if (G.K1 == 1) { sk = o.s2; flat = true; }
+        else if (G.K2 == 1) { sk = o.s1; flat = true; }
+        else { sk = o.s2; flat = o.s1 == (int64_t)G.K2 * o.s2; }
+    };
+    int64_t ak, bk;
+    bool af, bf;
+    kstride(G.A, ak, af);
+    kstride(G.B, bk, bf);
+    const bool flat = af && bf;
+    const int K = flat ? G.K1 * G.K2 : G.K2;
+    const int calls = flat ? 1 : G.K1;
+    cublasOperation_t ta, tb;
+    int64_t lda, ldb;
+    if (bk == 1) { ta = CUBLAS_OP_T; lda = G.B.s0; } else if (G.B.s0 == 1) { ta = CUBLAS_OP_N; lda = bk; } else return false;
+    if (ak == 1) { tb = CUBLAS_OP_N; ldb = G.A.s0; } else if (G.A.s0 == 1) { tb = CUBLAS_OP_T; ldb = ak; } else return false;
+    if (lda > INT32_MAX || ldb > INT32_MAX || G.C.s0 > INT32_MAX) return false;
+    if (cb.set_stream(h, st) != CUBLAS_STATUS_SUCCESS) return false;
+    const float** pa = (const float**)ptrs;
+    const float** pb = pa + max_batches;
+    float** pc = reinterpret_cast<float**>(ptrs + 2 * max_batches);
+    for (int k1 = 0; k1 < calls; ++k1) {
+        const int64_t a_off = flat ? 0 : (int64_t)k1 * G.A.s1, b_off = flat ? 0 : (int64_t)k1 * G.B.s1;
+        fill_ptrs<<<(unsigned)((batches + 255) / 256), 256, 0, st>>>(G, a_off, b_off, pa, pb, pc, batches);
+        const float alpha = G.alpha, beta = (G.acc || k1 > 0) ? 1.f : 0.f;
+        if (cb.gemm(h, ta, tb, G.N, G.M, K, &alpha, (const void* const*)pb, CUDA_R_32F, (int)lda,
+                    (const void* const*)pa, CUDA_R_32F, (int)ldb, &beta,
+                    (void* const*)pc, CUDA_R_32F, (int)G.C.s0, (int)batches,
+                    CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT) != CUBLAS_STATUS_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
 // ------------------------------------------------------------------ host
 struct Buf {
     int64_t* strides;   // q, k, v, out element strides (read by the gather / scatter kernels)
@@ -274,6 +386,8 @@ struct Buf {
     float *aL, *Y, *daL, *dY, *Ah, *dAh;
     float *cR, *dcL, *dcR;
     float *dL, *dLp, *z, *dR;
+    void** ptrs;        // 3 x max_batches pointers (cuBLAS batched calls)
+    int64_t max_batches;
 };
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -312,6 +426,10 @@ size_t layout(const Geometry& g, char* base, Buf* b) {
     x.dL = carve(pairs * s1);
     x.z = carve(pairs * s2);
     x.dR = carve(pairs * s2);
+    // the largest batch count of any call is bh gq gk max(s1, s2)
+    x.max_batches = (int64_t)bh * gq * gk * (s1 > s2 ? s1 : s2);
+    x.ptrs = base ? reinterpret_cast<void**>(base + off) : nullptr;
+    off += align_up((size_t)x.max_batches * 3 * sizeof(void*));
     if (b) *b = x;
     return off;
 }
@@ -320,6 +438,9 @@ struct Ctx {
     const Geometry& g;
     cudaStream_t st;
     cudaError_t err = cudaSuccess;
+    bool tf32 = false;          // bf16 I/O: TF32 tensor-core GEMMs through cuBLAS
+    void** ptrs = nullptr;
+    int64_t max_batches = 0;
 };
 
 Operand op(const float* p, int64_t s0, int64_t s1, int64_t s2, int64_t b0, int64_t b1, int64_t b2, int64_t b3) {
@@ -345,8 +466,12 @@ void gemm(Ctx& c, const char* name, int M, int N, int K1, int K2, const int nb[4
     G.alpha = alpha;
     G.acc = acc;
     const int64_t batches = (int64_t)nb[0] * nb[1] * nb[2] * nb[3];
-    dim3 grid((unsigned)(batches * ((N + kTN - 1) / kTN)), (unsigned)((M + kTM - 1) / kTM));
     ProfScope p(name, c.st);
+    if (c.tf32 && gemm_tf32(G, c.ptrs, c.max_batches, c.st)) {
+        c.err = cudaGetLastError();
+        return;
+    }
+    dim3 grid((unsigned)(batches * ((N + kTN - 1) / kTN)), (unsigned)((M + kTM - 1) / kTM));
     gemm_batched<<<grid, kGemmThreads, 0, c.st>>>(G);
     c.err = cudaGetLastError();
 }
@@ -359,6 +484,9 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
     Buf b;
     layout(g, ws, &b);
     Ctx c{g, stream};
+    c.tf32 = sizeof(T) == 2;
+    c.ptrs = b.ptrs;
+    c.max_batches = b.max_batches;
     const int64_t bh = g.bh, gq = g.gq, gk = g.gk, s1 = g.s1, s2 = g.s2, d = g.d, dv = g.dv;
     const int64_t bha = bh * gq;
     const int64_t tq = gq * s1 * s2, tk = gk * s1 * s2;
