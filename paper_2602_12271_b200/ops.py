@@ -301,6 +301,29 @@ def plan_key(low: Lowered) -> str:
     return key
 
 
+def _plan_fields(plan) -> tuple:
+    """A TilePlan / BlockConfig as a tuple of primitives (Dynamo can pass those as constants;
+    it cannot reconstruct frozen dataclass instances)."""
+    cfg = plan.config if isinstance(plan, TilePlan) else plan
+    s = cfg.shape
+    head = (s.f, s.h, s.w, cfg.b1, cfg.b2, cfg.g1, cfg.g2)
+    if isinstance(plan, TilePlan):
+        return ("tile",) + head + (plan.c1, plan.c2, plan.neighborhoods)
+    return ("block",) + head
+
+
+@torch._dynamo.assume_constant_result
+def _traced_plan_key(fields: tuple, q_tokens: int, kv_tokens: int, kv_frames) -> str:
+    """Plan lowering for a traced call: host-side numpy work on graph constants, run once
+    at trace time (Dynamo records the resulting key string, it does not trace into it)."""
+    from .layout import VideoShape
+
+    kind, f, h, w, b1, b2, g1, g2 = fields[:8]
+    cfg = BlockConfig(VideoShape(f, h, w), b1, b2, g1, g2)
+    plan = TilePlan(cfg, fields[8], fields[9], fields[10]) if kind == "tile" else cfg
+    return plan_key(lower_for(plan, q_tokens, kv_tokens, kv_frames))
+
+
 @torch.library.custom_op("monarch_b200::monarch_attention", mutates_args=())
 def _monarch_op(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, plan: str, iterations: int,
                 scale: float) -> torch.Tensor:
@@ -340,12 +363,14 @@ def monarch_attention(q, k, v, plan, iterations: int = 1, scale: float | None = 
     Eager calls go straight to the C ABI; under torch.compile tracing, or when
     autograd needs a graph, the call goes through the registered custom op.
     """
-    low = lower_for(plan, q.shape[2], k.shape[2], kv_frames)
     traced = torch.compiler.is_compiling()
     needs_grad = torch.is_grad_enabled() and (q.requires_grad or k.requires_grad or v.requires_grad)
     if (traced or needs_grad) and not (return_factors or force_generic or out is not None):
         sc = float(scale) if scale is not None else 1.0 / math.sqrt(q.shape[3])
-        return torch.ops.monarch_b200.monarch_attention(q, k, v, plan_key(low), iterations, sc)
+        key = _traced_plan_key(_plan_fields(plan), q.shape[2], k.shape[2], kv_frames) if traced else \
+            plan_key(lower_for(plan, q.shape[2], k.shape[2], kv_frames))
+        return torch.ops.monarch_b200.monarch_attention(q, k, v, key, iterations, sc)
+    low = lower_for(plan, q.shape[2], k.shape[2], kv_frames)
     return forward(q, k, v, low, iterations, scale, out=out, return_factors=return_factors,
                    force_generic=force_generic)
 
