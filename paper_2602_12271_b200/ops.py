@@ -204,14 +204,46 @@ def forward(q, k, v, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_
     return out
 
 
+BACKWARD_MAX_BYTES = 8 << 30   # device memory one backward call may hold (workspace + factors)
+
+
+def _backward_bytes_per_head(q, k, v, low: Lowered, iterations) -> int:
+    """Workspace + recomputed factors of one (b,h) head of the backward."""
+    lib = _lib.load()
+    q1, k1, v1 = q[:1, :1], k[:1, :1], v[:1, :1]
+    prep = prepare(q1, k1, v1, q1, low, iterations)
+    ws = lib.mbx_backward_workspace_bytes(ctypes.byref(prep.desc))
+    pairs = low.c1_q * low.c2 * low.c1_kv * low.c2
+    fac = iterations * pairs * (low.s2 * low.s1 * low.s1 + low.s1 * low.s2 * low.s2) * 4
+    return int(ws) + int(fac)
+
+
 def backward(q, k, v, dout, low: Lowered, iterations=1, scale=None, eps_div=1e-30, eps_log=1e-300,
-             factors=None):
+             factors=None, max_bytes=None):
     """Gradients (dq, dk, dv) of sum(out * dout) through ``mbx_backward``.
 
     ``factors`` = (L', R') of every refinement as returned by
     ``forward(..., return_factors=True, all_iters=True)``; recomputed when absent
-    (FlashAttention-style recomputation: the forward is cheap next to the backward)."""
+    (FlashAttention-style recomputation: the forward is cheap next to the backward).
+    With recomputation the (b,h) heads are processed in chunks whose workspace and
+    factors stay under ``max_bytes`` (default ``BACKWARD_MAX_BYTES``): the paper's
+    mini-sequence chunking for training, e.g. the Wan stack at B=8."""
     lib = _lib.load()
+    if factors is None:
+        B, H = q.shape[:2]
+        cap = max_bytes if max_bytes is not None else BACKWARD_MAX_BYTES
+        per = B * H if cap == float("inf") else \
+            max(1, int(cap) // max(1, _backward_bytes_per_head(q, k, v, low, iterations)))
+        if per < B * H:
+            flat = [x.reshape(1, B * H, x.shape[2], x.shape[3]) for x in (q, k, v, dout)]
+            grads = [torch.empty(x.shape, dtype=x.dtype, device=x.device) for x in flat[:3]]
+            for lo in range(0, B * H, per):
+                hi = min(B * H, lo + per)
+                part = backward(*(x[:, lo:hi] for x in flat), low, iterations, scale, eps_div, eps_log,
+                                max_bytes=float("inf"))
+                for g_, p_ in zip(grads, part):
+                    g_[:, lo:hi].copy_(p_)
+            return tuple(g_.view(x.shape) for g_, x in zip(grads, (q, k, v)))
     if factors is None:
         _, lf, rf = forward(q, k, v, low, iterations, scale, eps_div, eps_log, return_factors=True,
                             all_iters=True)

@@ -129,3 +129,21 @@ def test_all_iteration_factor_export(cuda, dtype, T):
         torch.cuda.synchronize()
         assert torch.equal(lf[t], l1), t
         assert torch.equal(rf[t], r1), t
+
+
+def test_backward_head_chunks_equal_one_call(cuda):
+    """Mini-sequence chunking of the backward (recompute + gradients per chunk of (b,h)
+    heads under a memory cap) gives the one-call gradients (to TF32 round-off: cuBLAS
+    may pick another batched kernel for another batch count)."""
+    s = pk.VideoShape(3, 30, 52)
+    plan = pk.make_tile_plan(s, pk.aligned_config(s, ("f", "h")), (1, 30, 52))
+    low = pk.lower_square(plan)
+    g = torch.Generator(device="cpu").manual_seed(9)
+    q, k, v, dout = (torch.randn(2, 3, 4680, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(4))
+    full = ops.backward(q, k, v, dout, low, 1, max_bytes=float("inf"))
+    per = ops._backward_bytes_per_head(q, k, v, low, 1)
+    chunked = ops.backward(q, k, v, dout, low, 1, max_bytes=2 * per + 1)   # chunks of 2 heads
+    torch.cuda.synchronize()
+    for a, b in zip(full, chunked):
+        err = ((a.float() - b.float()).norm() / a.float().norm()).item()
+        assert err < 2e-3, err
