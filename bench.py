@@ -620,6 +620,18 @@ def run_ours(args):
             ach = byts / t_s / 1e9
             roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peaks["hbm"],
                         "unit": "GB/s", "frac": round(ach / peaks["hbm"], 4)}
+        # The two-stage design moves the [aL | Y] exchange (SURVEY.md §8d "intermediate
+        # materialisation") through L2: bytes including it, against the measured L2 read
+        # bandwidth for working sets beyond 48 MB (scripts/microbench.cu,
+        # profiles/r1_microbench_memory.json) -- the bound the stages actually run into.
+        if wl["T"] == 1 and ("row" in kname or "column" in kname):
+            exch = units * (low.c1_q * low.c2) * (low.c1_kv * low.c2) * low.s1 * low.s2 * ((wl["d"] + wl["dv"]) * eb + 4)
+            l2b = byts + exch
+            l2_peak = _l2_peak()
+            if l2_peak:
+                roofline["exchange_l2"] = {"bytes_per_launch": int(l2b), "achieved": round(l2b / t_s / 1e9, 1),
+                                           "peak": l2_peak, "unit": "GB/s", "frac": round(l2b / t_s / 1e9 / l2_peak, 4),
+                                           "peak_source": "L2 read GB/s, >= 48 MB working set, profiles/r1_microbench_memory.json"}
         roofline.update({"kernel": kname, "traffic": _ncu_traffic(kname, name),
                          "peak_source": f"{peaks['src']} (MEASURED_PEAKS.json burst)",
                          "algorithmic_flops_per_launch": int(flops), "algorithmic_bytes_per_launch": int(byts),
@@ -789,6 +801,17 @@ def _self_launch(args):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     os.execv(sys.executable, cmd)
+
+
+def _l2_peak():
+    """Measured L2 read bandwidth (GB/s) for working sets beyond the L2-resident sweet spot."""
+    p = os.path.join(ROOT, "profiles", "r1_microbench_memory.json")
+    try:
+        with open(p) as fh:
+            rd = json.load(fh)["l2_read_GBps"]
+        return float(min(v for kk, v in rd.items() if int(kk) >= 48))
+    except Exception:
+        return None
 
 
 def _ncu_traffic(kernel, config):
