@@ -7,7 +7,9 @@
 //   softmax (warps 2-5, thread = query row l): bias -c_L, online max with lazy
 //   rescaling of its own O row in TMEM, P = 2^(x - m) as bf16 into TMEM
 //   MMA_O  O[l, v] += P[l, keys] . Y[keys, v]            128 x 128 x 128  (A = P in TMEM)
-// i.e. FlashAttention over the keys (c, k) of one column with the c_L bias
+// i.e. FlashAttention over the keys (c, k) of one column with the c_L bias.  The softmax
+// reads a thread's 128 scores in one TMEM round trip (four loads, one wait) and keeps them
+// in registers for the max and the exponentials (two passes over TMEM cost 3-7 % at N=32k)
 // (solver.py:192-195 joint softmax; factors.py:124 O = L Y).  mode 1 writes the
 // row statistics (max, 1/sum) instead of O (refinements t < T-1).
 constexpr int kWideThreads = 192;
@@ -212,23 +214,26 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
                 mbar_wait(&s_full[sb], (u >> 1) & 1);
                 tc_fence_after();
                 const uint32_t srow = tmem + kWS + sb * 128 + lane_off;
-                // pass 1: chunk max of x = S sl2 - c_L log2e over the valid keys
-                float mx = -1e30f;
-#pragma unroll 1
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    float x[32];
-                    tmem_ld32(srow + q4 * 32, x);
+                // one TMEM round trip for the whole 128-key row: x = S sl2 - c_L log2e in registers
+                float x[kWKC];
+                {
+                    uint32_t* xr = reinterpret_cast<uint32_t*>(x);
 #pragma unroll
-                    for (int k4 = 0; k4 < 32; k4 += 4) {
-                        const float4 c4 = ld_shared_v4f(cbuf + (q4 * 32 + k4) * 4);
-                        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+                    for (int q4 = 0; q4 < 4; ++q4) tmem_ld32_nw(srow + q4 * 32, xr + q4 * 32);
+                    tmem_wait_ld();
+                }
+                float mq[4] = {-1e30f, -1e30f, -1e30f, -1e30f};
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float xv = fmaf(x[k4 + e], sl2, -cv[e] * kLog2e);
-                            mx = (q4 * 32 + k4 + e < kvalid) ? fmaxf(mx, xv) : mx;
-                        }
+                for (int k4 = 0; k4 < kWKC; k4 += 4) {
+                    const float4 c4 = ld_shared_v4f(cbuf + k4 * 4);
+                    const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        x[k4 + e] = (k4 + e < kvalid) ? fmaf(x[k4 + e], sl2, -cv[e] * kLog2e) : -1e30f;
+                        mq[e] = fmaxf(mq[e], x[k4 + e]);
                     }
                 }
+                const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
                 // lazy online max: keep m_run unless the chunk max exceeds it by > 8 (x 256)
                 if (ch == 0) {
                     m_run = mx;
@@ -249,29 +254,23 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
                         }
                     }
                 }
-                // pass 2: P = 2^(x - m) (0 for padded keys) as bf16 pairs into TMEM
+                // P = 2^(x - m) (0 for padded keys) as bf16 pairs into TMEM
                 if (outm && u >= 2) mbar_wait(&o_done[sb], ((u - 2) >> 1) & 1);   // MMA_O(u-2) done with P buffer sb
                 float ssum = 0.f;
-#pragma unroll 1
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    float x[32];
-                    tmem_ld32(srow + q4 * 32, x);
-                    uint32_t pk[16];
+                {
+                    float sq[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                    for (int k4 = 0; k4 < 32; k4 += 4) {
-                        const float4 c4 = ld_shared_v4f(cbuf + (q4 * 32 + k4) * 4);
-                        const float cv[4] = {c4.x, c4.y, c4.z, c4.w};
-                        float pv[4];
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        uint32_t pk[16];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float xv = fmaf(x[k4 + e], sl2, -cv[e] * kLog2e);
-                            pv[e] = (q4 * 32 + k4 + e < kvalid) ? ex2(xv - m_run) : 0.f;
-                            ssum += pv[e];
+                        for (int k2 = 0; k2 < 32; k2 += 2) {
+                            const float p0 = ex2(x[q4 * 32 + k2] - m_run), p1 = ex2(x[q4 * 32 + k2 + 1] - m_run);
+                            sq[(k2 >> 1) & 3] += p0 + p1;
+                            pk[k2 >> 1] = pack_bf16(p0, p1);
                         }
-                        pk[k4 / 2] = pack_bf16(pv[0], pv[1]);
-                        pk[k4 / 2 + 1] = pack_bf16(pv[2], pv[3]);
+                        if (outm) tmem_st16(tmem + kWP + sb * 64 + lane_off + q4 * 16, pk);
                     }
-                    if (outm) tmem_st16(tmem + kWP + sb * 64 + lane_off + q4 * 16, pk);
+                    ssum = (sq[0] + sq[1]) + (sq[2] + sq[3]);
                 }
                 s_run += ssum;
                 tc_fence_before();
