@@ -260,15 +260,11 @@ tc_row_flash(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wa
                 const int kvalid = min(kFKC, g.s2 - ch * kFKC);
                 float mx = -1e30f;
                 float z[128];
-                {
-                    uint32_t zr[32];
+                {   // the four 32-column loads in flight before one wait
+                    uint32_t* zr = reinterpret_cast<uint32_t*>(z);
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        tmem_ld32_nw(sbuf + q4 * 32, zr);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) z[q4 * 32 + i] = __uint_as_float(zr[i]);
-                    }
+                    for (int q4 = 0; q4 < 4; ++q4) tmem_ld32_nw(sbuf + q4 * 32, zr + q4 * 32);
+                    tmem_wait_ld();
                 }
                 if (kvalid < kFKC) {
 #pragma unroll
