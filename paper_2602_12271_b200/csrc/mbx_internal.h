@@ -84,6 +84,7 @@ struct Options {
     int fusedhand = 1;  // T >= 2: alpha_R hand-off inside the column stage when a column is one key chunk
     int wave = -1;      // (b, h) slices per wave of the tensor-core path: -1 from the cap, 0 one wave
     int ws_cap_mb = 2048;   // automatic waves keep the tensor-core workspace under this many MiB
+    int wide2 = 1;          // output pass of the wide column stage with two item streams per CTA (0: one)
     unsigned version = 0;   // bumped on every change (keys the launch-parameter cache)
 };
 const Options& options();

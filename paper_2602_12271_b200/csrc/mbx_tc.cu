@@ -111,6 +111,7 @@ __device__ __forceinline__ void store_r_row(float* dst, const float* p, float in
 #include "mbx_tc_col.cuh"
 #include "mbx_tc_alpha.cuh"
 #include "mbx_tc_colw.cuh"
+#include "mbx_tc_colw2.cuh"
 #include "mbx_tc_rowp.cuh"
 #include "mbx_tc_rowf.cuh"
 
@@ -253,6 +254,7 @@ static void init_options() {
     g_opts.fusedhand = env("MBX_FUSEDHAND", 1);
     g_opts.wave = env("MBX_WAVE", -1);
     g_opts.ws_cap_mb = env("MBX_WS_CAP_MB", 2048);
+    g_opts.wide2 = env("MBX_WIDE2", 1);
 }
 
 const Options& options() {
@@ -268,7 +270,7 @@ int set_option(const char* name, int value) {
         {"MBX_PDL", &g_opts.pdl}, {"MBX_L2HINT", &g_opts.l2hint}, {"MBX_DBG", &g_opts.dbg},
         {"MBX_PAIR", &g_opts.pair}, {"MBX_WIDE", &g_opts.wide}, {"MBX_SPLIT", &g_opts.split},
         {"MBX_VERBOSE", &g_opts.verbose}, {"MBX_FUSEDHAND", &g_opts.fusedhand},
-        {"MBX_WAVE", &g_opts.wave}, {"MBX_WS_CAP_MB", &g_opts.ws_cap_mb}};
+        {"MBX_WAVE", &g_opts.wave}, {"MBX_WS_CAP_MB", &g_opts.ws_cap_mb}, {"MBX_WIDE2", &g_opts.wide2}};
     for (auto& t : tab)
         if (strcmp(t.n, name) == 0) {
             const int prev = *t.p;
@@ -557,6 +559,7 @@ static cudaError_t ensure_attributes(int dev) {
         {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage<0>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_stage<1>, ColSmem::kTotal + 1024}, {(const void*)tc_column_stage<2>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
+        {(const void*)tc_column_wide2, Wide2Smem::kTotal + 1024},
         {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}, {(const void*)tc_row_flash, RowFSmem::kTotal + 1024}};
     for (auto& x : k)
         if ((e = cudaFuncSetAttribute(x.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x.smem)) != cudaSuccess)
@@ -600,6 +603,11 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
         return le;
     };
     auto column = [&](int mode, TcParams& Pc) -> cudaError_t {
+        if (T.wide && mode == 0 && options().wide2 != 0) {   // two item streams per CTA (ping-pong)
+            ProfScope p("tc_column_wide", stream);
+            void* args[] = {(void*)&Pc, (void*)&g};
+            return launch((const void*)tc_column_wide2, T.grid_wide, kW2Threads, Wide2Smem::kTotal + 1024, args);
+        }
         if (T.wide) {
             ProfScope p("tc_column_wide", stream);
             void* args[] = {(void*)&Pc, (void*)&g, (void*)&mode};
