@@ -272,6 +272,17 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 }
 
 // Named barrier over `count` threads (ids 1..15; 0 is __syncthreads).
+// Warpgroup register reallocation (all four warps of the warpgroup execute it, at the top
+// of the warpgroup's branch so ptxas can budget the code after it).
+template <int N>
+__device__ __forceinline__ void reg_alloc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_dealloc() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __device__ __forceinline__ void named_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }

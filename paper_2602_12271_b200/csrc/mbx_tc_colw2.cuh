@@ -5,7 +5,7 @@
 // overlap the other's score MMA: the CTA's items alternate between streams s = 0, 1;
 // stream s owns TMEM columns [256 s, 256 s + 256) -- S (fp32, 128 columns) with P
 // written over it in place as packed bf16, then O (128 columns) -- and softmax warps
-// 2 + 4 s .. 5 + 4 s.
+// 4 + 4 s .. 7 + 4 s.
 //
 // One global step list interleaves the streams' chunks, (s0,c0) (s1,c0) (s0,c1) ...;
 // the MMA warp issues MMA_S of step k before MMA_O of step k-1 unless both belong to
@@ -13,7 +13,9 @@
 // of a stream's chunk c therefore also covers its MMA_O of chunk c-1, so the softmax
 // may rescale O and overwrite P as soon as it sees the new scores.  The producer
 // loads in exactly the MMA order (aL for S, Y for O) through one 3-slot ring.
-constexpr int kW2Threads = 320;   // producer, MMA, 2 x 4 softmax / output warps
+// Warpgroups: [producer, MMA, 2 idle] at 48 registers, then one softmax / output
+// warpgroup per stream at 224 (setmaxnreg), so the 128-score rows stay in registers.
+constexpr int kW2Threads = 384;
 struct Wide2Smem {
     static constexpr int kQ = 0;                    // Q tiles [2 streams][2 d-chunks][128 rows][128 B] (64 KB)
     static constexpr int kNRing = 3;
@@ -129,7 +131,9 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
         if (pending >= 0) visit(true, pending);
     };
 
-    if (warp == 0) {
+    if (warp < 4) {
+      reg_dealloc<48>();
+      if (warp == 0) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
         const uint64_t w_policy = P.l2hint ? l2_evict_first() : l2_evict_normal();   // W's last reader
@@ -228,14 +232,16 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
             __syncwarp();
             ++n;
         });
+      }
     } else {
+        reg_alloc<224>();
         // ------------------------------------------ softmax (thread = query row l) + output, stream s
-        const int s = (warp - 2) >> 2;
+        const int s = (warp - 4) >> 2;
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t sp = tmem + (uint32_t)s * 256 + lane_off;
         const float sl2 = g.scale * kLog2e;
-        uint8_t* stg = smem + Wide2Smem::kStage + (warp - 2) * 4096;
+        uint8_t* stg = smem + Wide2Smem::kStage + (warp - 4) * 4096;
         const int n_items = s == 0 ? (my_items + 1) / 2 : my_items / 2;
         int c = 0;
         for (int i = 0; i < n_items; ++i) {
