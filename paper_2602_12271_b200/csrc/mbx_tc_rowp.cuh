@@ -193,10 +193,6 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         };
         PairCursor pc = cur;
         while (pc.valid) {
-            if (amode || pc.first_of_item(t0)) {
-                load_a(pc);
-                if (leader) TR(0, ti, 1);
-            }
             const int b = pc.bh / g.heads, h = pc.bh % g.heads;
             int kvi = pc.kvi, kst = pc.kst, kph = pc.kph;
             for (int r = 0; r < pc.nrows(); ++r) {
@@ -218,6 +214,11 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                     kst = 0;
                     kph ^= 1;
                 }
+            }
+            // the task's K/V rows go out before its A rows: an A issue can block ~1 us (C2 -1 %)
+            if (amode || pc.first_of_item(t0)) {
+                load_a(pc);
+                if (leader) TR(0, ti, 1);
             }
             pc.advance();
         }
