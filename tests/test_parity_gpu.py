@@ -252,6 +252,34 @@ def test_wide_column_path(cuda, frames, q_frames, nb, H, T):
     assert orc.rel_l2(out.float().cpu().numpy(), ref) < BF16_TOL
 
 
+@pytest.mark.parametrize("frames,q_frames,nb,T", [(3, 3, (3, 30, 52), 1), (6, 3, (3, 30, 52), 2), (7, 7, None, 1),
+                                                  (5, 5, "raw", 1), (3, 3, None, 1)])
+def test_wide_column_ping_pong_vs_single_stream(cuda, mbx_option, frames, q_frames, nb, T):
+    """The output pass of the wide column stage, two item streams per CTA (tc_column_wide2,
+    the default) against the single-stream kernel (MBX_WIDE2=0): same softmax arithmetic,
+    per-chunk O accumulation order identical, so equal up to the MMA's bf16 rounding of P;
+    odd and even item counts per CTA, one and several key chunks per column."""
+    g = torch.Generator(device="cpu").manual_seed(frames * 11 + q_frames + 7 * T)
+    h, w = 30, 52
+    q = torch.randn(1, 3, q_frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    k = torch.randn(1, 3, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    v = torch.randn(1, 3, frames * h * w, 128, generator=g).to(cuda, torch.bfloat16)
+    shape = pk.VideoShape(frames, h, w)
+    if nb is None:
+        low = pk.lower_square(pk.aligned_config(shape, ("f", "h")))
+    elif nb == "raw":
+        low = pk.lower_square(pk.config_from_sizes(shape, 300, 26))
+    else:
+        plan = pk.make_tile_plan(shape, pk.aligned_config(shape, ("f", "h")), nb)
+        low = pk.lower_chunked(plan, q_frames) if q_frames != frames else pk.lower_square(plan)
+    assert low.s1 > 32
+    two = ops.forward(q, k, v, low, T).clone()
+    mbx_option("MBX_WIDE2", 0)
+    one = ops.forward(q, k, v, low, T)
+    torch.cuda.synchronize()
+    assert orc.rel_l2(two.float().cpu().numpy(), one.float().cpu().numpy()) < 2e-3
+
+
 @pytest.mark.parametrize("row_stage", ["0", "1"])
 @pytest.mark.parametrize("frames,q_frames,h,nb,T", [(3, 3, 30, None, 1), (5, 3, 30, None, 2), (2, 2, 30, None, 1),
                                                     (4, 4, 30, None, 1), (3, 3, 30, (3, 30, 52), 1),
