@@ -559,7 +559,8 @@ static cudaError_t ensure_attributes(int dev) {
         {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage<0>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_stage<1>, ColSmem::kTotal + 1024}, {(const void*)tc_column_stage<2>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
-        {(const void*)tc_column_wide2, Wide2Smem::kTotal + 1024},
+        {(const void*)tc_column_wide2<0>, Wide2Smem::kTotal + 1024},
+        {(const void*)tc_column_wide2<1>, Wide2Smem::kTotal + 1024},
         {(const void*)tc_row_pair, RowPSmem::kTotal + 1024}, {(const void*)tc_row_flash, RowFSmem::kTotal + 1024}};
     for (auto& x : k)
         if ((e = cudaFuncSetAttribute(x.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, x.smem)) != cudaSuccess)
@@ -603,10 +604,11 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
         return le;
     };
     auto column = [&](int mode, TcParams& Pc) -> cudaError_t {
-        if (T.wide && mode == 0 && options().wide2 != 0) {   // two item streams per CTA (ping-pong)
+        if (T.wide && mode <= 1 && options().wide2 != 0) {   // two item streams per CTA (ping-pong)
             ProfScope p("tc_column_wide", stream);
             void* args[] = {(void*)&Pc, (void*)&g};
-            return launch((const void*)tc_column_wide2, T.grid_wide, kW2Threads, Wide2Smem::kTotal + 1024, args);
+            const void* fn = mode == 0 ? (const void*)tc_column_wide2<0> : (const void*)tc_column_wide2<1>;
+            return launch(fn, T.grid_wide, kW2Threads, Wide2Smem::kTotal + 1024, args);
         }
         if (T.wide) {
             ProfScope p("tc_column_wide", stream);

@@ -1,4 +1,5 @@
-// Wide column stage, ping-pong variant (included by mbx_tc.cu; output mode only).
+// Wide column stage, ping-pong variant (included by mbx_tc.cu).  mode 0: O = L Y;
+// mode 1 (refinements t < T-1): the row statistics (max, 1/sum) of L only, no Y, no O.
 // Same FlashAttention over the keys (c, k) of one column as tc_column_wide
 // (mbx_tc_colw.cuh, solver.py:192-195 joint softmax with bias -c_L, factors.py:124
 // O = L Y), with two item streams per CTA so one softmax warpgroup's exponentials
@@ -44,8 +45,10 @@ struct W2Steps {
     __device__ __forceinline__ int total() const { return u0 + u1; }
 };
 
+template <int mode>
 __global__ void __launch_bounds__(kW2Threads, 1)
 tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
+    constexpr bool outm = mode == 0;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Wide2Smem::kBars);
@@ -115,6 +118,10 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
     // the op sequence shared by producer and MMA issuer: S(k) preceded by O(k-1) when both
     // are of one stream, followed by it otherwise; visit(is_o, step)
     auto schedule = [&](auto&& visit) {
+        if (!outm) {   // statistics: score MMAs only
+            for (int k = 0; k < K; ++k) visit(false, k);
+            return;
+        }
         int pending = -1, ps = -1;
         for (int k = 0; k < K; ++k) {
             int s, c;
@@ -136,7 +143,7 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
       if (warp == 0) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
-        const uint64_t w_policy = P.l2hint ? l2_evict_first() : l2_evict_normal();   // W's last reader
+        const uint64_t w_policy = P.l2hint && outm ? l2_evict_first() : l2_evict_normal();   // W's last reader
         uint32_t n = 0;   // ring uses
         bool waited = false;
         schedule([&](bool is_o, int k) {
@@ -201,6 +208,9 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
             const int sl = n % Wide2Smem::kNRing;
             if (!is_o) {
                 if (ch == 0) mbar_wait(q_full(s), i & 1);
+                // statistics mode has no MMA_O between a stream's score MMAs: S(c) may only
+                // overwrite S(c-1) once the softmax read it
+                if (!outm && c > 0) mbar_wait(p_full(s), (c - 1) & 1);
                 mbar_wait(&r_full[sl], (n / Wide2Smem::kNRing) & 1);
                 tc_fence_after();
                 if (leader) {
@@ -263,6 +273,10 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
                     for (int q4 = 0; q4 < 4; ++q4) tmem_ld32_nw(sp + q4 * 32, xr + q4 * 32);
                     tmem_wait_ld();
                 }
+                if (!outm) {   // scores in registers: the next score MMA of this stream may start
+                    tc_fence_before();
+                    mbar_arrive(p_full(s));
+                }
                 float mq[4] = {-1e30f, -1e30f, -1e30f, -1e30f};
 #pragma unroll
                 for (int k4 = 0; k4 < kWKC; k4 += 4) {
@@ -283,7 +297,7 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
                     m_run = mx;
                     s_run *= fac;
 #pragma unroll 1
-                    for (int q4 = 0; q4 < 4; ++q4) {   // this thread's O row
+                    for (int q4 = 0; q4 < (outm ? 4 : 0); ++q4) {   // this thread's O row
                         float o[32];
                         tmem_ld32(sp + 128 + q4 * 32, o);
 #pragma unroll
@@ -302,12 +316,19 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
                         sq[(k2 >> 1) & 3] += p0 + p1;
                         pk[k2 >> 1] = pack_bf16(p0, p1);
                     }
-                    tmem_st16(sp + q4 * 16, pk);
+                    if (outm) tmem_st16(sp + q4 * 16, pk);
                 }
                 s_run += (sq[0] + sq[1]) + (sq[2] + sq[3]);
                 tc_fence_before();
                 mbar_arrive(c_empty(s, cb));
-                mbar_arrive(p_full(s));
+                if (outm) mbar_arrive(p_full(s));
+            }
+            if (!outm) {   // L statistics of row l (log2 units)
+                if (l < g.s1) {
+                    P.stats[(int64_t)col * P.stats_pitch + l] = m_run;
+                    P.stats[(int64_t)col * P.stats_pitch + P.stats_pitch / 2 + l] = 1.f / s_run;
+                }
+                continue;
             }
             // output row l: O[l, :] / s_run -> bf16 -> staging -> TMA store (rows at stride W tokens)
             mbar_wait(o_full(s), i & 1);
