@@ -85,7 +85,6 @@ struct TcParams {
     float* stats;                         // T >= 2: per (col, l) running max and 1/sum of L
     int stats_pitch;                      // floats per column: [max x s1p | 1/sum x s1p]
     CUtensorMap tqcw, toutw;              // wide column stage: q columns (128 rows), output rows (32 x 64)
-    CUtensorMap tws16, tws16r;            // paired row stage: workspace stores of 16 / (s2 % 16) columns
     CUtensorMap tqa;                      // alpha_R stage: q columns, s1 rounded up to 32 rows
     __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
     int64_t out_bh_stride, out_tok_stride;
