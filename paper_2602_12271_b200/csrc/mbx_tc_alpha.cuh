@@ -15,7 +15,13 @@
 // normalised P^T = L is needed; each thread writes its key's L[l] for every query
 // row l straight into L' (c1_q, c2, c1_kv, c2, s2, s1, s1) (factors.py:57-79) and
 // MMA2 / the alpha_R epilogue are skipped.
-constexpr int kAlphaThreads = 192;   // producer, MMA, 4 x softmax / epilogue
+#ifndef MBX_ALPHA_PP
+#define MBX_ALPHA_PP 1
+#endif
+// MBX_ALPHA_PP: two softmax / epilogue warpgroups, items alternating (warpgroup b owns the
+// S^T / D2 / P^T buffers of parity b), so one item's epilogue overlaps the next's softmax;
+// the epilogue stages its stores in the item's own P^T buffer, which MMA2 has finished with
+constexpr int kAlphaThreads = MBX_ALPHA_PP ? 320 : 192;   // producer, MMA, (1 or 2) x 4 softmax / epilogue
 constexpr int kAKC = 128;            // keys per item
 struct AlphaSmem {
     // per buffer b (2): aL [2 d-chunks][128 keys][128 B] (32 KB), Q_col [2 d-chunks][128 l][128 B]
@@ -144,18 +150,25 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             }
             __syncwarp();
         }
-    } else if (warp < 6) {
+    } else if (warp < kAlphaThreads / 32) {
         // ------------------------------------------ softmax (thread = key) + epilogue
         const int quad = warp & 3;
         const int r = quad * 32 + lane;   // key within the chunk
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const float sl2 = g.scale * kLog2e;
-        uint8_t* stg_base = smem + AlphaSmem::kStage + quad * 4096;
-        for (int it = 0; it < my_items; ++it) {
+        const int wgi = MBX_ALPHA_PP ? (warp - 2) >> 2 : 0;
+        for (int it = wgi; it < my_items; it += (MBX_ALPHA_PP ? 2 : 1)) {
             int col, ch;
             decode(it, col, ch);
             const int b = it & 1;
             uint8_t* base = smem + b * AlphaSmem::kBuf;
+            // epilogue staging: in the two-warpgroup layout the warp's own P^T rows of the item's
+            // buffer (4 KB in each 64-l chunk: only this warp writes them), else a 4 KB slot per warp
+            uint8_t* stg_base = MBX_ALPHA_PP ? base + AlphaSmem::kP + quad * 4096 : smem + AlphaSmem::kStage + quad * 4096;
+            if (MBX_ALPHA_PP) {   // this warp's stores from the buffer (item it-2) have read it
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+            }
             const int key = ch * kAKC + r;
             const bool key_ok = key < g.nkeys;
             // row statistics of this column (written by the statistics pass)
@@ -213,9 +226,11 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
                 float o[64];
                 tmem_ld32(tmem + 256 + b * 128 + lane_off + part * 64, o);
                 tmem_ld32(tmem + 256 + b * 128 + lane_off + part * 64 + 32, o + 32);
-                uint8_t* stg = stg_base;
-                if (lane == 0) bulk_wait_read<0>();
-                __syncwarp();
+                uint8_t* stg = stg_base + (MBX_ALPHA_PP ? part * 16384 : 0);
+                if (!MBX_ALPHA_PP) {
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+                }
                 const uint32_t srow = smem_u32(stg) + lane * 128;
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc)
