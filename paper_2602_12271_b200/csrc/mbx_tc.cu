@@ -555,7 +555,7 @@ static cudaError_t ensure_attributes(int dev) {
     if (done[dev]) return cudaSuccess;
     cudaError_t e;
     const struct { const void* fn; int smem; } k[] = {
-        {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage<0>, ColSmem::kTotal + 1024},
+        {(const void*)tc_row_stage, RowSmem::kTotal + 1024},     {(const void*)tc_column_stage<0>, ColSmemT<0>::kTotal + 1024},
         {(const void*)tc_column_stage<1>, ColSmem::kTotal + 1024}, {(const void*)tc_column_stage<2>, ColSmem::kTotal + 1024},
         {(const void*)tc_column_wide, WideSmem::kTotal + 1024},  {(const void*)tc_alpha_r_stage, AlphaSmem::kTotal + 1024},
         {(const void*)tc_column_wide2<0>, Wide2Smem::kTotal + 1024},
@@ -618,7 +618,7 @@ static cudaError_t tc_forward_one(const Geometry& g0, int flags, const void* q, 
         void* args[] = {(void*)&Pc, (void*)&g};
         const void* fn = mode == 0 ? (const void*)tc_column_stage<0>
                          : mode == 1 ? (const void*)tc_column_stage<1> : (const void*)tc_column_stage<2>;
-        return launch(fn, T.grid_col, kColThreads, T.smem_col, args);
+        return launch(fn, T.grid_col, kColThreads, mode == 0 ? ColSmemT<0>::kTotal + 1024 : T.smem_col, args);
     };
     auto alpha = [&](int amode, TcParams& Pc) -> cudaError_t {
         ProfScope p(amode ? "tc_alpha_l_export" : "tc_alpha_r_stage", stream);

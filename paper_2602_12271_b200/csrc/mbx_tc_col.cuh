@@ -14,20 +14,28 @@
 // (solver.py:192-195 joint softmax with bias -c_L; factors.py:124 O = L Y).
 constexpr int kColThreads = 192;   // 6 warps: producer, MMA, 4 x softmax/output
 constexpr int kKC = 96;            // keys per chunk (S_i is 96 TMEM columns)
-constexpr int kRing = 5;           // aL / Y chunk slots
-struct ColSmem {
+#ifndef MBX_COL_RING6
+#define MBX_COL_RING6 1
+#endif
+// MBX_COL_RING6: six ring slots, paid for by one output staging buffer per warp (reused
+// column by column) instead of four
+template <int mode>
+struct ColSmemT {
+    static constexpr bool kSix = MBX_COL_RING6 && mode == 0;   // mode 2 needs the 4-column staging
+    static constexpr int kRing = kSix ? 6 : 5;           // aL / Y chunk slots
     static constexpr int kQ = 0;                          // Qstack: 2 d-chunks x [128][64] (32 KB)
     static constexpr int kSlot = 2 * kKC * 128;           // [96 keys][128 feat] as 2 x [96][64] (24 KB)
     static constexpr int kRingOff = 32768;
     static constexpr int kP = kRingOff + kRing * kSlot;   // P_i: 2 x [32 l][64 keys] (8 KB each)
     static constexpr int kC = kP + 4 * 8192;              // c_L chunks: [4 columns][2 buffers] x 96 floats (512 B pitch)
     static constexpr int kOut = kC + 8 * 512;             // output staging [4 warps][4 columns] x [32 rows][64 B]
-    static constexpr int kStat = kOut + 16 * 2048;        // row sums [4][32], rescale [4][32], flags [4], rb[32]
+    static constexpr int kStat = kOut + (kSix ? 4 : 16) * 2048;   // row sums [4][32], rescale [4][32], flags [4], rb[32]
     static constexpr int kBars = kStat + 4 * 32 * 4 * 2 + 4 * 4 + 32 * 8;
     static constexpr int kNumBars = 2 * kRing + 2 + 4 * 4 + 1 + 16;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
+using ColSmem = ColSmemT<1>;
 
 // Column-stage role of CTA `first` among `stride` column CTAs.
 // mode 0: O = L Y (last refinement); mode 1 (T >= 2, earlier refinements): only the
@@ -41,6 +49,9 @@ struct ColSmem {
 // max(c_R, eps) (bf16) for the next row stage -- no statistics pass, no alpha_R stage.
 template <int mode>   // compile-time: each mode gets its own register allocation
 __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const Geometry& g, int first, int stride) {
+    using ColSmem = ColSmemT<mode>;
+    constexpr int kRing = ColSmem::kRing;
+    constexpr bool kSix = ColSmem::kSix;
     constexpr bool outm = mode == 0;
     constexpr bool hand = mode == 2;
     const CUtensorMap& tm_w = P.tw;
@@ -537,7 +548,12 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                 }
                 if (j0 + i < g.s2) {
                     // rows l of column j: smem [l][64 B] (this warp's value dims), one TMA store
-                    const uint32_t stg = smem_u32(smem + ColSmem::kOut + (quad * 4 + i) * 2048) + lane * 2;
+                    const int ob = kSix ? quad : quad * 4 + i;
+                    if (kSix && i > 0) {   // one buffer per warp: the previous column's store read it
+                        if (lane == 0) bulk_wait_read<0>();
+                        __syncwarp();
+                    }
+                    const uint32_t stg = smem_u32(smem + ColSmem::kOut + ob * 2048) + lane * 2;
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
                         const __nv_bfloat16 hv = __float2bfloat16_rn(o[q] * inv[q]);
@@ -549,7 +565,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
                     __syncwarp();
                     if (lane == 0) {
                         const int64_t tok = tok0 + i;
-                        tma_store_4d(&tm_out, smem + ColSmem::kOut + (quad * 4 + i) * 2048, quad * 32,
+                        tma_store_4d(&tm_out, smem + ColSmem::kOut + ob * 2048, quad * 32,
                                      (int)(tok % g.W), (int)(tok / g.W), bh);
                         bulk_commit();
                     }
