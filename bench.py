@@ -67,6 +67,14 @@ CONFIGS = {
                  "C4d N=32760 untiled misaligned raw (b1,b2) = (1260,26)"),
     "n32k_f": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("f",)), "bf16",
                "C4e N=32760 untiled aligned (f, hw) = (21,1560) (long tile rows: online-softmax row stage)"),
+    "n32k_w": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("w",)), "bf16",
+               "C4f N=32760 untiled aligned (w, fh) = (52,630) (permuted plan: gathered into slot order)"),
+    "n32k_hw": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("h", "w")), "bf16",
+                "C4g N=32760 untiled aligned (hw, f) = (1560,21) (permuted plan: gathered into slot order)"),
+    "n32k_fw": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("f", "w")), "bf16",
+                "C4h N=32760 untiled aligned (fw, h) = (1092,30) (permuted plan: gathered into slot order)"),
+    "n32k_h": (1, 12, 21, 21, 30, 52, 128, ("aligned", ("h",)), "bf16",
+               "C4i N=32760 untiled aligned (h, fw) = (30,1092) (permuted plan: gathered into slot order)"),
     "sf720": (1, 12, 3, 3, 45, 80, 128, (1, 45, 80), "bf16",
               "720p Self-Forcing chunk: B=1 H=12, 3 frames x (45,80), (h,w)-tiled (PAPER.md:866 shapes)"),
     "sf720_3hw": (1, 12, 3, 3, 45, 80, 128, (3, 45, 80), "bf16",

@@ -231,6 +231,44 @@ bool column_grid(const Geometry& g, int* F, int* H, int* W) {
     return true;
 }
 
+// The geometry of a permuted plan's gathered copy: q, k, v (and out) in slot order, one
+// contiguous (b h) slab of rows of 128 features each, identity orders.
+Geometry slot_geometry(const Geometry& g) {
+    Geometry s = g;
+    const int64_t nq = (int64_t)g.c1q * g.s1 * g.c2 * g.s2, nk = (int64_t)g.c1k * g.s1 * g.c2 * g.s2;
+    s.q_order = s.kv_order = nullptr;
+    s.qs[0] = (int64_t)g.heads * nq * kD; s.qs[1] = nq * kD; s.qs[2] = kD;
+    s.os[0] = s.qs[0]; s.os[1] = s.qs[1]; s.os[2] = s.qs[2];
+    s.ks[0] = (int64_t)g.heads * nk * kD; s.ks[1] = nk * kD; s.ks[2] = kD;
+    s.vs[0] = s.ks[0]; s.vs[1] = s.ks[1]; s.vs[2] = s.ks[2];
+    return s;
+}
+size_t gather_bytes(const Geometry& g) {
+    const size_t nq = (size_t)g.c1q * g.s1 * g.c2 * g.s2, nk = (size_t)g.c1k * g.s1 * g.c2 * g.s2;
+    return align256((size_t)g.bh * (2 * nq + 2 * nk) * kD * 2);
+}
+
+// dst[bh][p][:] = src[b, h, order[p], :] (or the reverse with scatter): 16 threads per 256-byte row
+__global__ void gather_rows(const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                            const int32_t* __restrict__ order, int64_t n, int bh, int heads, int64_t s0, int64_t s1,
+                            int64_t s2, int scatter) {
+    const int64_t total = (int64_t)bh * n * 16;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i & 15);
+        const int64_t row = i >> 4;
+        const int64_t p = row % n;
+        const int u = (int)(row / n);
+        const int b = u / heads, h = u - (u / heads) * heads;
+        const int64_t tok = order ? order[p] : p;
+        const uint4* a = reinterpret_cast<const uint4*>(src + b * s0 + h * s1 + tok * s2) + c;
+        uint4* slot = reinterpret_cast<uint4*>(dst + row * kD) + c;
+        if (scatter)
+            *const_cast<uint4*>(a) = *slot;
+        else
+            *slot = *a;
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ options
@@ -288,15 +326,21 @@ static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags
     if (factors && g.s2 > kMaxS2) return "factor export with s2 > 64";   // online row softmax (flash row stage)
     if (g.T > 1 && g.s1 > 128) return "T > 1 with s1 > 128";   // alpha_R hand-off: query rows l on the MMA N axis
     if (factors && g.s1 > 128) return "factor export with s1 > 128";   // L export shares the alpha_R kernel
-    if (g.nf == 0 && (g.q_order || g.kv_order)) return "permuted plan without a closed form";
+    // permuted plans without a closed form (the aligned (w, fh), (hw, f), (fw, h), (h, fw)
+    // configurations, misaligned raw orders) run gathered into slot order (tc_forward), where
+    // the identity plan's tile rows are contiguous -- possible when c2 == 1
+    const bool gathered = g.nf == 0 && (g.q_order || g.kv_order);
+    if (gathered && g.c2 != 1) return "permuted plan with c2 > 1 and no closed form";
+    Geometry gs = g;
+    if (gathered) gs = slot_geometry(g);
     int F, H, W;
-    if (!column_grid(g, &F, &H, &W)) return "tile rows are not contiguous grid rows";
+    if (!column_grid(gs, &F, &H, &W)) return "tile rows are not contiguous grid rows";
     if (!strides_ok(g.qs) || !strides_ok(g.ks) || !strides_ok(g.vs) || !strides_ok(g.os))
         return "strides not 16-byte aligned";
     // the q-column / output maps fold (b, h) into one dim; a size-1 batch has no stride to fold
     // (PyTorch keeps the parent's batch stride on head slices of a B = 1 tensor)
-    if (g.bh > g.heads && g.qs[0] != (int64_t)g.heads * g.qs[1]) return "q batch stride != heads * head stride";
-    if (g.bh > g.heads && g.os[0] != (int64_t)g.heads * g.os[1]) return "out batch stride != heads * head stride";
+    if (gs.bh > gs.heads && gs.qs[0] != (int64_t)gs.heads * gs.qs[1]) return "q batch stride != heads * head stride";
+    if (gs.bh > gs.heads && gs.os[0] != (int64_t)gs.heads * gs.os[1]) return "out batch stride != heads * head stride";
     if ((int64_t)g.bh * g.gq * g.s2 * g.nkeys >= ((int64_t)1 << 31)) return "workspace rows exceed 2^31";
     if (encode_fn() == nullptr) return "cuTensorMapEncodeTiled unavailable";
     return nullptr;
@@ -750,9 +794,15 @@ static size_t tc_wave_bytes(const Geometry& g, int flags) {
     return tc_layout(wave_geom(g, w.nb, w.nh)).total;
 }
 
-size_t tc_workspace_bytes(const Geometry& g, int flags) {
+static size_t tc_workspace_bytes_ordered(const Geometry& g, int flags) {
     if (tc_split(g, flags)) return 2 * align256(tc_wave_bytes(half_heads(g), flags));
     return tc_wave_bytes(g, flags);
+}
+
+size_t tc_workspace_bytes(const Geometry& g, int flags) {
+    if (g.nf == 0 && (g.q_order || g.kv_order))   // gathered copies + the slot-order problem
+        return gather_bytes(g) + tc_workspace_bytes_ordered(slot_geometry(g), flags);
+    return tc_workspace_bytes_ordered(g, flags);
 }
 
 // One launch sequence per wave, in (batch, head) order on `stream`; later waves use PDL
@@ -823,8 +873,50 @@ static SideStream* side_for(int dev, cudaStream_t caller, bool may_create) {
     return &g_sides[g_nsides++];
 }
 
+static cudaError_t tc_forward_ordered(const Geometry& g, int flags, const void* q, const void* k, const void* v,
+                                      void* out, float* l_factor, float* r_factor, void* workspace, cudaStream_t stream);
+
 cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* k, const void* v, void* out,
                        float* l_factor, float* r_factor, void* workspace, cudaStream_t stream) {
+    if (!(g.nf == 0 && (g.q_order || g.kv_order)))
+        return tc_forward_ordered(g, flags, q, k, v, out, l_factor, r_factor, workspace, stream);
+    // permuted plan: gather q / k / v into slot order (the reference's q[order], solver.py:103-106),
+    // run the identity-order problem, scatter the output back (attention_output, solver.py:216)
+    const Geometry gs = slot_geometry(g);
+    const int64_t nq = (int64_t)g.c1q * g.s1 * g.c2 * g.s2, nk = (int64_t)g.c1k * g.s1 * g.c2 * g.s2;
+    __nv_bfloat16* qg = reinterpret_cast<__nv_bfloat16*>(workspace);
+    __nv_bfloat16* og = qg + (size_t)g.bh * nq * kD;
+    __nv_bfloat16* kg = og + (size_t)g.bh * nq * kD;
+    __nv_bfloat16* vg = kg + (size_t)g.bh * nk * kD;
+    char* rest = reinterpret_cast<char*>(workspace) + gather_bytes(g);
+    int dev = 0;
+    cudaError_t e0 = cudaGetDevice(&dev);
+    if (e0 != cudaSuccess) return e0;
+    if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) return TC_FAIL("tensor map / argument check");
+    const int grid = num_sms(dev) * 4;
+    {
+        ProfScope p("tc_gather", stream);
+        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(q), qg, g.q_order, nq, g.bh,
+                                              g.heads, g.qs[0], g.qs[1], g.qs[2], 0);
+        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(k), kg, g.kv_order, nk, g.bh,
+                                              g.heads, g.ks[0], g.ks[1], g.ks[2], 0);
+        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(v), vg, g.kv_order, nk, g.bh,
+                                              g.heads, g.vs[0], g.vs[1], g.vs[2], 0);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = tc_forward_ordered(gs, flags, qg, kg, vg, og, l_factor, r_factor, rest, stream);
+    if (e != cudaSuccess) return e;
+    {
+        ProfScope p("tc_scatter", stream);
+        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(out), og, g.q_order, nq, g.bh,
+                                              g.heads, g.os[0], g.os[1], g.os[2], 1);
+    }
+    return cudaGetLastError();
+}
+
+static cudaError_t tc_forward_ordered(const Geometry& g, int flags, const void* q, const void* k, const void* v,
+                                      void* out, float* l_factor, float* r_factor, void* workspace, cudaStream_t stream) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

@@ -185,3 +185,19 @@ def test_long_tile_rows_flash_row_stage(cuda, name, fhw, kind, q_frames, T, H):
         _, _, ref = _oracle(q, k, v, low, T, 0, h)
         err = orc.rel_l2(out[0, h].float().cpu().numpy(), ref)
         assert err < BF16_TOL, (name, h, err)
+
+
+@pytest.mark.parametrize("g1", [("f", "h"), ("w",), ("f",), ("h", "w"), ("f", "w"), ("h",)])
+def test_all_aligned_configs_n32k_tensor_cores(cuda, g1):
+    """All six aligned (b1, b2) configurations of the N=32760 (21, 30, 52) grid
+    (enumerate_aligned_configs, layout.py:252-276; BASELINE.json config 4's aligned
+    sweep) select the tensor-core path -- the permuted ones gathered into slot order --
+    and match the oracle on one head at T = 1."""
+    shape = pk.VideoShape(21, 30, 52)
+    low = pk.lower_square(pk.aligned_config(shape, g1))
+    q, k, v = _inputs(zlib.crc32(repr(g1).encode()) & 0xFFFF, 1, shape.n, shape.n, cuda)
+    assert ops.selected_path(q, k, v, low, 1) == "tcgen05", g1
+    out = ops.forward(q, k, v, low, 1)
+    _, _, ref = _oracle(q, k, v, low, 1)
+    err = orc.rel_l2(out[0, 0].float().cpu().numpy(), ref)
+    assert err < BF16_TOL, (g1, err)

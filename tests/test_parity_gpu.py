@@ -435,3 +435,26 @@ def test_split_side_streams_are_per_caller_stream(cuda):
             ops.forward(qb, kb, vb, low, 1, out=ob, split=True)
     torch.cuda.synchronize()
     assert torch.equal(oa, ra) and torch.equal(ob, rb)
+
+
+@pytest.mark.parametrize("T", [1, 2])
+def test_permuted_aligned_configs_gathered(cuda, T):
+    """Every aligned (b1, b2) configuration of a 3 x 30 x 52 grid (enumerate_aligned_configs,
+    layout.py:252-276) -- including the permuted ones whose tile rows are not contiguous token
+    runs ((w, fh), (hw, f), (fw, h), (h, fw)): those run gathered into slot order on the
+    tensor cores -- against the oracle; T = 2 where the alpha_R hand-off applies (s1 <= 128)."""
+    shape = pk.VideoShape(3, 30, 52)
+    g = torch.Generator(device="cpu").manual_seed(21 + T)
+    q, k, v = (torch.randn(1, 1, shape.n, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    seen = 0
+    for cfg in pk.enumerate_aligned_configs(shape):
+        low = pk.lower_square(cfg)
+        if T > 1 and low.s1 > 128:
+            continue
+        assert ops.selected_path(q, k, v, low, T) == "tcgen05", (cfg.g1, cfg.g2)
+        out = ops.forward(q, k, v, low, T)
+        ref = _oracle_heads(q, k, v, low, T)
+        err = orc.rel_l2(out.float().cpu().numpy(), ref)
+        assert err < BF16_TOL, (cfg.g1, cfg.g2, err)
+        seen += 1
+    assert seen >= (6 if T == 1 else 3)
