@@ -1,6 +1,6 @@
 // tcgen05 / TMEM / TMA kernels of the tiled MonarchAttention forward (bf16,
 // d = d_v = 128, tile rows of <= 64 tokens, any number of tiles, any T; T >= 2
-// and factor export need s1 <= 128).  Warp-specialized persistent kernels
+// and factor export step over rows in chunks of 128).  Warp-specialized persistent kernels
 // joined by a bf16 workspace W[b,h,a,j,(c,k),0:256] = [aL | Y] and c_L
 // (SURVEY.md Appendix B):
 //   row stage    (mbx_tc_row.cuh, mbx_tc_rowp.cuh)  solver.py:187-191, factors.py:123
@@ -324,8 +324,6 @@ static const char* tc_unsupported_reason(const Geometry& g, int dtype, int flags
     if (flags & MBX_FLAG_NO_OUTPUT) return "factors without output";
     if (dtype != MBX_BF16 || g.d != kD || g.dv != kD || g.T < 1) return "needs bf16 with d = dv = 128";
     if (factors && g.s2 > kMaxS2) return "factor export with s2 > 64";   // online row softmax (flash row stage)
-    if (g.T > 1 && g.s1 > 128) return "T > 1 with s1 > 128";   // alpha_R hand-off: query rows l on the MMA N axis
-    if (factors && g.s1 > 128) return "factor export with s1 > 128";   // L export shares the alpha_R kernel
     // permuted plans without a closed form (the aligned (w, fh), (hw, f), (fw, h), (h, fw)
     // configurations, misaligned raw orders) run gathered into slot order (tc_forward), where
     // the identity plan's tile rows are contiguous -- possible when c2 == 1

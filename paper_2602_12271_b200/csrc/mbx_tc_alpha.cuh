@@ -30,7 +30,7 @@ struct AlphaSmem {
     static constexpr int kBuf = kC + 1024;               // keeps buffer 1 on a 1024 B (SW128) boundary
     static constexpr int kStage = 2 * kBuf;              // [4 warps] x [32 keys][64] bf16 (one slot each)
     static constexpr int kBars = kStage + 4 * 4096;
-    static constexpr int kNumBars = 10;
+    static constexpr int kNumBars = 12;
     static constexpr int kTmemSlot = kBars + kNumBars * 8;
     static constexpr int kTotal = kTmemSlot + 16;
 };
@@ -47,6 +47,7 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
     uint64_t* s_full = bars + 4;     // [2]
     uint64_t* p_full = bars + 6;     // [2]  128 softmax threads wrote P^T, read S^T
     uint64_t* o_full = bars + 8;     // [2]  (D2 buffer b; drained before the next s_full of b)
+    uint64_t* p_empty = bars + 10;   // [2]  MMA2 of a step done reading P^T (rows l beyond 128: next step)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + AlphaSmem::kTmemSlot);
     const int tid = threadIdx.x, lane = tid & 31;
     const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
@@ -66,12 +67,17 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
             mbar_init(&o_full[i], 1);
+            mbar_init(&p_empty[i], 1);
         }
         fence_barrier_init();
     }
     // l padded to s1p (multiple of 32): Q_col rows >= s1 (TMA loads s1p rows: finite data or OOB
     // zeros) meet P^T columns that are written as zeros below, so nothing needs pre-zeroing.
+    // Rows l beyond 128 (untiled / misaligned plans) run in steps of 128 l per item: S^T, P^T and
+    // Q_col per step, alpha_R accumulated in D2 across the steps, c_R in registers.
     const int s1p = ((g.s1 + 31) / 32) * 32;
+    const int nlc = (s1p + 127) / 128;                  // l steps per item
+    auto step_l = [&](int lc) { return min(128, s1p - lc * 128); };   // rows l of step lc
     if (warp == 0) tmem_alloc<512>(tmem_slot);
     fence_proxy_async_smem();
     tc_fence_before();
@@ -94,61 +100,76 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             int col, ch;
             decode(it, col, ch);
             const int b = it & 1;
-            mbar_wait(&ld_empty[b], ((it >> 1) & 1) ^ 1);
             const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
             const int64_t tok = row_base(g, true, a, 0) + j;
             const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
-            if (leader) {
-                uint8_t* base = smem + b * AlphaSmem::kBuf;
-                // q columns: s1p rows only (MMA1's N and MMA2's K stop there)
-                mbar_expect_tx(&ld_full[b], 2u * kAKC * 128u + 2u * (uint32_t)s1p * 128u + kAKC * 4u);
-                tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
-                tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
-                tma_load_4d(base + AlphaSmem::kQc, &P.tqa, &ld_full[b], 0, wcol, wrow, bh);
-                tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqa, &ld_full[b], 64, wcol, wrow, bh);
-                tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
+            for (int lc = 0; lc < nlc; ++lc) {
+                const int sidx = (it >> 1) * nlc + lc;   // step of buffer b
+                mbar_wait(&ld_empty[b], (sidx & 1) ^ 1);
+                if (leader) {
+                    uint8_t* base = smem + b * AlphaSmem::kBuf;
+                    // q columns: one box of min(s1p, 128) rows (tensor map P.tqa) per step -- a
+                    // full box even on the last step (rows past the column are zero-filled, and
+                    // MMA1's N / MMA2's K stop at the step's rows)
+                    const uint32_t qbytes = 2u * (uint32_t)(s1p < 128 ? s1p : 128) * 128u;
+                    mbar_expect_tx(&ld_full[b], qbytes + (lc == 0 ? 2u * kAKC * 128u + kAKC * 4u : 0u));
+                    if (lc == 0) {
+                        tma_load_4d(base + AlphaSmem::kA, &P.tw128, &ld_full[b], 0, ch * kAKC, 0, col);
+                        tma_load_4d(base + AlphaSmem::kA + 16384, &P.tw128, &ld_full[b], 0, ch * kAKC, 1, col);
+                        tma_load_2d(base + AlphaSmem::kC, &P.tc128, &ld_full[b], ch * kAKC, col);
+                    }
+                    tma_load_4d(base + AlphaSmem::kQc, &P.tqa, &ld_full[b], 0, wcol, wrow + lc * 128, bh);
+                    tma_load_4d(base + AlphaSmem::kQc + 16384, &P.tqa, &ld_full[b], 64, wcol, wrow + lc * 128, bh);
+                }
+                __syncwarp();
             }
-            __syncwarp();
         }
     } else if (warp == 1) {
         // ------------------------------------------ MMA issuer (whole warp, uniform descriptors)
         const bool leader = elect_one();
-        const uint32_t id1 = idesc_bf16(128, s1p, false, false);
         const uint32_t id2 = idesc_bf16(128, 128, false, true);
         constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
         auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
         const uint32_t base_lo = (smem_u32(smem) & 0x3FFFF) >> 4;
         for (int it = 0; it < my_items; ++it) {
             const int b = it & 1;
-            mbar_wait(&ld_full[b], (it >> 1) & 1);
-            // S^T buffer b free: the softmax of item it-2 read it (p_full(it-2) precedes it)
-            if (it >= 2) mbar_wait(&p_full[b], ((it >> 1) - 1) & 1);
-            tc_fence_after();
             const uint32_t lo = base_lo + (uint32_t)b * (AlphaSmem::kBuf >> 4);
-            if (leader) {
+            for (int lc = 0; lc < nlc; ++lc) {
+                const int sidx = (it >> 1) * nlc + lc;
+                const int nl = step_l(lc);
+                mbar_wait(&ld_full[b], sidx & 1);
+                // S^T buffer b free: the softmax read the previous step's S^T (p_full precedes it)
+                if (sidx >= 1) mbar_wait(&p_full[b], (sidx - 1) & 1);
+                tc_fence_after();
+                if (leader) {
+                    const uint32_t id1 = idesc_bf16(128, nl, false, false);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk)
-                    mma_bf16(tmem + b * 128, desc(lo + ((AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
-                             desc(lo + ((AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)), id1,
-                             kk > 0);
-                mma_commit(&s_full[b]);
+                    for (int kk = 0; kk < 8; ++kk)
+                        mma_bf16(tmem + b * 128, desc(lo + ((AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                                 desc(lo + ((AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)), id1,
+                                 kk > 0);
+                    mma_commit(&s_full[b]);
+                }
+                __syncwarp();
+                // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
+                // which the softmax threads finish before arriving on p_full)
+                mbar_wait(&p_full[b], sidx & 1);
+                tc_fence_after();
+                if (leader && lexp) {   // L export: no alpha_R product (and no o_full: nobody drains D2)
+                    mma_commit(&ld_empty[b]);
+                    if (lc < nlc - 1) mma_commit(&p_empty[b]);   // waited by the item's next step only
+                } else if (leader) {
+                    for (int kk = 0; kk < nl / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
+                        mma_bf16(tmem + 256 + b * 128,
+                                 desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                                 desc(lo + ((AlphaSmem::kQc + kk * 2048) >> 4) + (16384u >> 4 << 16)), id2,
+                                 lc > 0 || kk > 0);
+                    if (lc == nlc - 1) mma_commit(&o_full[b]);
+                    mma_commit(&ld_empty[b]);
+                    if (lc < nlc - 1) mma_commit(&p_empty[b]);
+                }
+                __syncwarp();
             }
-            __syncwarp();
-            // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
-            // which the softmax threads finish before arriving on p_full(it))
-            mbar_wait(&p_full[b], (it >> 1) & 1);
-            tc_fence_after();
-            if (leader && lexp) {   // L export: no alpha_R product (and no o_full: nobody drains D2)
-                mma_commit(&ld_empty[b]);
-            } else if (leader) {
-                for (int kk = 0; kk < s1p / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
-                    mma_bf16(tmem + 256 + b * 128,
-                             desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
-                             desc(lo + ((AlphaSmem::kQc + kk * 2048) >> 4) + (16384u >> 4 << 16)), id2, kk > 0);
-                mma_commit(&o_full[b]);
-                mma_commit(&ld_empty[b]);
-            }
-            __syncwarp();
         }
     } else if (warp < kAlphaThreads / 32) {
         // ------------------------------------------ softmax (thread = key) + epilogue
@@ -173,10 +194,8 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
             const bool key_ok = key < g.nkeys;
             // row statistics of this column (written by the statistics pass)
             const float* st = P.stats + (int64_t)col * P.stats_pitch;
-            mbar_wait(&s_full[b], (it >> 1) & 1);
-            tc_fence_after();
-            const float cl = reinterpret_cast<const float*>(base + AlphaSmem::kC)[r] * kLog2e;
             float cr = 0.f;
+            float cl = 0.f;
             const uint32_t prow = smem_u32(base + AlphaSmem::kP) + r * 128;
             // L' row of this key: [bh][a][c][j][l][k] with key = c s1 + k
             float* lrow = nullptr;
@@ -185,39 +204,49 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
                 const int c = key / g.s1, kk = key - c * g.s1;
                 lrow = P.lfac + ((((int64_t)(bh * g.gq + a) * g.gk + c) * g.s2 + j) * g.s1) * g.s1 + kk;
             }
-            for (int l0 = 0; l0 < s1p; l0 += 32) {   // 32 query rows l per pass
-                float x[32];
-                tmem_ld32(tmem + b * 128 + lane_off + l0, x);
-                float p[32];
+            for (int lc = 0; lc < nlc; ++lc) {
+                const int sidx = (it >> 1) * nlc + lc;
+                const int nl = step_l(lc);
+                mbar_wait(&s_full[b], sidx & 1);
+                tc_fence_after();
+                if (lc == 0) cl = reinterpret_cast<const float*>(base + AlphaSmem::kC)[r] * kLog2e;
+                // P^T of the previous step read by its MMA2 (the first step's region was last
+                // read by item it-2's MMA2, complete before that item's epilogue)
+                if (lc > 0) mbar_wait(&p_empty[b], ((it >> 1) * (nlc - 1) + lc - 1) & 1);
+                for (int l0 = 0; l0 < nl; l0 += 32) {   // 32 query rows l per pass
+                    float x[32];
+                    tmem_ld32(tmem + b * 128 + lane_off + l0, x);
+                    float p[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int l = l0 + i;
-                    const float e = ex2(fmaf(x[i], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
-                    p[i] = (l < g.s1 && key_ok) ? e : 0.f;
-                    cr += p[i];
-                }
-                if (lrow) {
+                    for (int i = 0; i < 32; ++i) {
+                        const int l = lc * 128 + l0 + i;
+                        const float e = ex2(fmaf(x[i], sl2, -cl) - __ldg(st + l)) * __ldg(st + P.stats_pitch / 2 + l);
+                        p[i] = (l < g.s1 && key_ok) ? e : 0.f;
+                        cr += p[i];
+                    }
+                    if (lrow) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (l0 + i < g.s1) lrow[(int64_t)(l0 + i) * g.s1] = p[i];
-                }
-                if (lexp) continue;
-                // P^T row (keys on rows, l along K): 64-l chunk l0 / 64, logical 16 B chunks (l0 % 64) / 8 ..
-                const uint32_t pr = prow + (l0 >> 6) * 16384;
+                        for (int i = 0; i < 32; ++i)
+                            if (lc * 128 + l0 + i < g.s1) lrow[(int64_t)(lc * 128 + l0 + i) * g.s1] = p[i];
+                    }
+                    if (lexp) continue;
+                    // P^T row (keys on rows, l along K): 64-l chunk l0 / 64, logical 16 B chunks (l0 % 64) / 8 ..
+                    const uint32_t pr = prow + (l0 >> 6) * 16384;
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) {
-                    const int lc = ((l0 & 63) >> 3) + cc;
-                    st_shared_v4(pr + ((lc ^ (r & 7)) << 4), pack_bf16(p[8 * cc], p[8 * cc + 1]),
-                                 pack_bf16(p[8 * cc + 2], p[8 * cc + 3]), pack_bf16(p[8 * cc + 4], p[8 * cc + 5]),
-                                 pack_bf16(p[8 * cc + 6], p[8 * cc + 7]));
+                    for (int cc = 0; cc < 4; ++cc) {
+                        const int lq = ((l0 & 63) >> 3) + cc;
+                        st_shared_v4(pr + ((lq ^ (r & 7)) << 4), pack_bf16(p[8 * cc], p[8 * cc + 1]),
+                                     pack_bf16(p[8 * cc + 2], p[8 * cc + 3]), pack_bf16(p[8 * cc + 4], p[8 * cc + 5]),
+                                     pack_bf16(p[8 * cc + 6], p[8 * cc + 7]));
+                    }
                 }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(&p_full[b]);
             }
-            fence_proxy_async_smem();
-            tc_fence_before();
-            mbar_arrive(&p_full[b]);
             if (lexp) continue;
             // epilogue of this item: hat_alpha_R[key, :] = D2[key, :] / max(c_R, eps)
-            mbar_wait(&o_full[b], (it >> 1) & 1);
+            mbar_wait(&o_full[b], (it >> 1) & 1);   // one o_full per item
             tc_fence_after();
             const float inv = 1.f / fmaxf(cr, g.eps_div);
             const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;

@@ -201,3 +201,19 @@ def test_all_aligned_configs_n32k_tensor_cores(cuda, g1):
     _, _, ref = _oracle(q, k, v, low, 1)
     err = orc.rel_l2(out[0, 0].float().cpu().numpy(), ref)
     assert err < BF16_TOL, (g1, err)
+
+
+@pytest.mark.parametrize("name,g1,T", [("n32k_fhw", ("f", "h"), 2), ("n32k_hw", ("h", "w"), 2),
+                                       ("n32k_fw", ("f", "w"), 3)])
+def test_iterations_rows_beyond_128_n32k(cuda, name, g1, T):
+    """T >= 2 for untiled N=32760 plans with s1 = 630, 1560, 1092 rows per tile (the alpha_R
+    hand-off over rows l in steps of 128) on the tensor cores, against the oracle."""
+    shape = pk.VideoShape(21, 30, 52)
+    low = pk.lower_square(pk.aligned_config(shape, g1))
+    assert low.s1 > 128
+    q, k, v = _inputs(zlib.crc32(name.encode()) & 0xFFFF, 1, shape.n, shape.n, cuda)
+    assert ops.selected_path(q, k, v, low, T) == "tcgen05", name
+    out = ops.forward(q, k, v, low, T)
+    _, _, ref = _oracle(q, k, v, low, T)
+    err = orc.rel_l2(out[0, 0].float().cpu().numpy(), ref)
+    assert err < BF16_TOL, (name, err)

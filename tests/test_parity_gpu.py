@@ -442,19 +442,38 @@ def test_permuted_aligned_configs_gathered(cuda, T):
     """Every aligned (b1, b2) configuration of a 3 x 30 x 52 grid (enumerate_aligned_configs,
     layout.py:252-276) -- including the permuted ones whose tile rows are not contiguous token
     runs ((w, fh), (hw, f), (fw, h), (h, fw)): those run gathered into slot order on the
-    tensor cores -- against the oracle; T = 2 where the alpha_R hand-off applies (s1 <= 128)."""
+    tensor cores -- against the oracle, at T = 1 and 2 (the alpha_R hand-off steps over
+    rows l in chunks of 128 where s1 > 128)."""
     shape = pk.VideoShape(3, 30, 52)
     g = torch.Generator(device="cpu").manual_seed(21 + T)
     q, k, v = (torch.randn(1, 1, shape.n, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
     seen = 0
     for cfg in pk.enumerate_aligned_configs(shape):
         low = pk.lower_square(cfg)
-        if T > 1 and low.s1 > 128:
-            continue
         assert ops.selected_path(q, k, v, low, T) == "tcgen05", (cfg.g1, cfg.g2)
         out = ops.forward(q, k, v, low, T)
         ref = _oracle_heads(q, k, v, low, T)
         err = orc.rel_l2(out.float().cpu().numpy(), ref)
         assert err < BF16_TOL, (cfg.g1, cfg.g2, err)
         seen += 1
-    assert seen >= (6 if T == 1 else 3)
+    assert seen == 6
+
+
+@pytest.mark.parametrize("T", [2, 3])
+def test_factor_export_rows_beyond_128(cuda, T):
+    """Untiled (fh, w) plan with s1 = 150 > 128 rows per tile: the refinement hand-off and
+    the L' export step over rows l in chunks of 128 on the tensor cores; output and both
+    factors against the oracle."""
+    shape = pk.VideoShape(5, 30, 52)
+    low = pk.lower_square(pk.aligned_config(shape, ("f", "h")))
+    assert low.s1 == 150
+    g = torch.Generator(device="cpu").manual_seed(61 + T)
+    q, k, v = (torch.randn(1, 1, shape.n, 128, generator=g).to(cuda, torch.bfloat16) for _ in range(3))
+    assert ops.selected_path(q, k, v, low, T, return_factors=True) == "tcgen05"
+    out, lf, rf = ops.forward(q, k, v, low, T, return_factors=True)
+    qn, kn, vn = (x[0, 0].float().cpu().numpy().astype(np.float64) for x in (q, k, v))
+    idx = np.arange(low.n_q)
+    L, R, o = orc.forward_phi(qn, kn, vn, idx, idx, low.c1_q, low.c1_kv, low.c2, low.s1, low.s2, T)
+    assert orc.rel_l2(out[0, 0].float().cpu().numpy(), o) < BF16_TOL
+    assert orc.rel_l2(lf[0, 0].cpu().numpy(), L) < BF16_TOL
+    assert orc.rel_l2(rf[0, 0].cpu().numpy(), R) < BF16_TOL
