@@ -891,14 +891,15 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
     cudaError_t e0 = cudaGetDevice(&dev);
     if (e0 != cudaSuccess) return e0;
     if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) return TC_FAIL("tensor map / argument check");
-    const int grid = num_sms(dev) * 4;
+    // one 16-byte chunk per thread, no grid-stride loop: every load in flight at once
+    auto grid_for = [&](int64_t rows) { return (unsigned)((rows * 16 + 255) / 256); };
     {
         ProfScope p("tc_gather", stream);
-        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(q), qg, g.q_order, nq, g.bh,
+        gather_rows<<<grid_for(g.bh * nq), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(q), qg, g.q_order, nq, g.bh,
                                               g.heads, g.qs[0], g.qs[1], g.qs[2], 0);
-        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(k), kg, g.kv_order, nk, g.bh,
+        gather_rows<<<grid_for(g.bh * nk), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(k), kg, g.kv_order, nk, g.bh,
                                               g.heads, g.ks[0], g.ks[1], g.ks[2], 0);
-        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(v), vg, g.kv_order, nk, g.bh,
+        gather_rows<<<grid_for(g.bh * nk), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(v), vg, g.kv_order, nk, g.bh,
                                               g.heads, g.vs[0], g.vs[1], g.vs[2], 0);
     }
     cudaError_t e = cudaGetLastError();
@@ -907,7 +908,7 @@ cudaError_t tc_forward(const Geometry& g, int flags, const void* q, const void* 
     if (e != cudaSuccess) return e;
     {
         ProfScope p("tc_scatter", stream);
-        gather_rows<<<grid, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(out), og, g.q_order, nq, g.bh,
+        gather_rows<<<grid_for(g.bh * nq), 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(out), og, g.q_order, nq, g.bh,
                                               g.heads, g.os[0], g.os[1], g.os[2], 1);
     }
     return cudaGetLastError();

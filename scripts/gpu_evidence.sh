@@ -17,17 +17,18 @@ for a in "--config sf" "--config sf --iters 2" "--config sf --iters 3" "--config
          "--config kv21_3hw --iters 2" "--config kv21_3hw --iters 3" \
          "--config n32k" "--config n32k_3hw" "--config n32k_fhw" "--config n32k_mis" "--config n32k_f" "--config c1" \
          "--config sf720" "--config sf720_3hw" "--config kv21_720_3hw" "--config n75k_720_3hw" "--config wan --steps 2" \
-         "--config wan_3hw --steps 2"; do
+         "--config wan_3hw --steps 2" "--config n32k_w" "--config n32k_hw" "--config n32k_fw" "--config n32k_h" \
+         "--config n32k_fhw --iters 2" "--config n32k_mis --iters 2" "--config n32k_3hw --iters 2"; do
   timeout 900 python bench.py --steps 10 --warmup 3 $a --no-cpu --no-backward 2>/dev/null | tail -1 | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); d['args']='$a'; print(json.dumps(d))" >> gpurun_out/ev/sweep.jsonl
 done
-for spec in "sf 1" "sf3hw 1" "kv21 1" "sf 2"; do
-  set -- $spec; cfg=$1; it=$2; tag=${TAG:-r1d}_${cfg}_t${it}
+# spec: config, refinements, launches per forward (sf3hw T=2 = row, column statistics, alpha_R, row, column)
+for spec in "sf 1 2" "sf3hw 1 2" "kv21 1 2" "sf 2 4" "sf3hw 2 5"; do
+  set -- $spec; cfg=$1; it=$2; n=$3; tag=${TAG:-r1d}_${cfg}_t${it}
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tc_ --csv \
       --log-file gpurun_out/ev/${tag}_launches.csv python bench.py --config $cfg --iters $it --steps 5 --warmup 3 \
       --no-dense --no-cpu > gpurun_out/ev/${tag}_launches_bench.log 2>&1
-  n=$((it == 1 ? 2 : 3))
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_ -s $n -c $n \
       -o gpurun_out/ev/${tag} python scripts/profile_run.py $cfg 3 $it > gpurun_out/ev/${tag}_full.log 2>&1
 done
