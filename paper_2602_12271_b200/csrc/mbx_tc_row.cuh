@@ -293,12 +293,14 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
                     const int tok = (int)row_base(g, false, c, cur.kr);
                     if (leader) {
                         TR(0, ti, 2);
-                        mbar_expect_tx(&kv_full[ks], 4u * box_bytes);
+                        mbar_expect_tx(&kv_full[ks], (want_y ? 4u : 2u) * box_bytes);   // V only for Y
                         uint8_t* kb = smem + RowSmem::kKV + ks * RowSmem::kKVBytes;
                         tma_load_4d(kb, &tm_k, &kv_full[ks], 0, tok, h, b);
                         tma_load_4d(kb + 8192, &tm_k, &kv_full[ks], 64, tok, h, b);
-                        tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
-                        tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                        if (want_y) {
+                            tma_load_4d(kb + 16384, &tm_v, &kv_full[ks], 0, tok, h, b);
+                            tma_load_4d(kb + 24576, &tm_v, &kv_full[ks], 64, tok, h, b);
+                        }
                     }
                     __syncwarp();
                     if (amode)

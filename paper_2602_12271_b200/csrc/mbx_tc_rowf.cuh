@@ -161,13 +161,15 @@ tc_row_flash(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wa
                 const int st = n & 1;
                 mbar_wait(&kv_empty[st], ((n >> 1) & 1) ^ 1);
                 if (leader) {
-                    mbar_expect_tx(&kv_full[st], 65536u);
+                    mbar_expect_tx(&kv_full[st], want_y ? 65536u : 32768u);   // V only for Y
                     uint8_t* kb = smem + RowFSmem::kKV + st * RowFSmem::kKVStage;
                     const int tok = tokk + ch * kFKC;
                     tma_load_4d(kb, &P.tk128, &kv_full[st], 0, tok, h, b);
                     tma_load_4d(kb + 16384, &P.tk128, &kv_full[st], 64, tok, h, b);
-                    tma_load_4d(kb + 32768, &P.tv128, &kv_full[st], 0, tok, h, b);
-                    tma_load_4d(kb + 49152, &P.tv128, &kv_full[st], 64, tok, h, b);
+                    if (want_y) {
+                        tma_load_4d(kb + 32768, &P.tv128, &kv_full[st], 0, tok, h, b);
+                        tma_load_4d(kb + 49152, &P.tv128, &kv_full[st], 64, tok, h, b);
+                    }
                 }
                 __syncwarp();
             }

@@ -200,12 +200,14 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
                 // dbg 8 (timing only): every K/V load reads the same (L2-resident) row
                 const int tok = (P.dbg & 8) ? 0 : (int)row_base(g, false, pc.c, pc.kr(r));
                 if (leader) {
-                    mbar_expect_tx(&kv_full[kst], 4u * box_bytes);
+                    mbar_expect_tx(&kv_full[kst], (want_y ? 4u : 2u) * box_bytes);   // V only for Y
                     uint8_t* kb = smem + RowPSmem::kKV + kst * kvbytes;
                     tma_load_4d(kb, &P.tk, &kv_full[kst], 0, tok, h, b);
                     tma_load_4d(kb + cpitch, &P.tk, &kv_full[kst], 64, tok, h, b);
-                    tma_load_4d(kb + 2 * cpitch, &P.tv, &kv_full[kst], 0, tok, h, b);
-                    tma_load_4d(kb + 3 * cpitch, &P.tv, &kv_full[kst], 64, tok, h, b);
+                    if (want_y) {
+                        tma_load_4d(kb + 2 * cpitch, &P.tv, &kv_full[kst], 0, tok, h, b);
+                        tma_load_4d(kb + 3 * cpitch, &P.tv, &kv_full[kst], 64, tok, h, b);
+                    }
                 }
                 if (leader) TR(0, ti, 2);
                 __syncwarp();
