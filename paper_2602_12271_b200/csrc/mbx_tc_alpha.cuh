@@ -21,6 +21,9 @@
 // MBX_ALPHA_PP: two softmax / epilogue warpgroups, items alternating (warpgroup b owns the
 // S^T / D2 / P^T buffers of parity b), so one item's epilogue overlaps the next's softmax;
 // the epilogue stages its stores in the item's own P^T buffer, which MMA2 has finished with
+#ifndef MBX_ALPHA_IL
+#define MBX_ALPHA_IL 1   // interleave the steps of item pairs (build option, for A/B)
+#endif
 constexpr int kAlphaThreads = MBX_ALPHA_PP ? 320 : 192;   // producer, MMA, (1 or 2) x 4 softmax / epilogue
 constexpr int kAKC = 128;            // keys per item
 struct AlphaSmem {
@@ -92,18 +95,35 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
         ch = item % nch;
         col = item / nch;
     };
+    // Step order of the producer and the MMA warp: with two softmax warpgroups the steps of
+    // items 2g and 2g+1 interleave ((2g,0), (2g+1,0), (2g,1), ...), so one item's softmax,
+    // Q load and MMA2 overlap the other's; a trailing odd item runs alone.
+    const int nsteps = my_items * nlc;
+    auto seq = [&](int q, int& it, int& lc) {
+        const int paired = MBX_ALPHA_PP && MBX_ALPHA_IL ? (my_items & ~1) * nlc : 0;
+        if (q < paired) {
+            const int r = q % (2 * nlc);
+            it = 2 * (q / (2 * nlc)) + (r & 1);
+            lc = r >> 1;
+        } else {
+            const int q2 = q - paired;
+            it = (paired / nlc) + q2 / nlc;
+            lc = q2 % nlc;
+        }
+    };
 
     if (warp == 0) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
-        for (int it = 0; it < my_items; ++it) {
-            int col, ch;
+        for (int q = 0; q < nsteps; ++q) {
+            int it, lc, col, ch;
+            seq(q, it, lc);
             decode(it, col, ch);
             const int b = it & 1;
             const int bh = col / (g.gq * g.s2), a = (col / g.s2) % g.gq, j = col % g.s2;
             const int64_t tok = row_base(g, true, a, 0) + j;
             const int wcol = (int)(tok % g.W), wrow = (int)(tok / g.W);
-            for (int lc = 0; lc < nlc; ++lc) {
+            {
                 const int sidx = (it >> 1) * nlc + lc;   // step of buffer b
                 mbar_wait(&ld_empty[b], (sidx & 1) ^ 1);
                 if (leader) {
@@ -131,46 +151,72 @@ tc_alpha_r_stage(const __grid_constant__ TcParams P, Geometry g, int mode) {
         constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);   // SBO 1024, v1, SW128
         auto desc = [](uint32_t lo) { return ((uint64_t)kHi << 32) | lo; };
         const uint32_t base_lo = (smem_u32(smem) & 0x3FFFF) >> 4;
-        for (int it = 0; it < my_items; ++it) {
+        // MMA2 of step (it, lc), once the softmax wrote its P^T (and D2 buffer b was drained by
+        // item it-2's epilogue, which the softmax threads finish before arriving on p_full)
+        auto mma2 = [&](int it, int lc) {
             const int b = it & 1;
             const uint32_t lo = base_lo + (uint32_t)b * (AlphaSmem::kBuf >> 4);
-            for (int lc = 0; lc < nlc; ++lc) {
-                const int sidx = (it >> 1) * nlc + lc;
-                const int nl = step_l(lc);
-                mbar_wait(&ld_full[b], sidx & 1);
-                // S^T buffer b free: the softmax read the previous step's S^T (p_full precedes it)
-                if (sidx >= 1) mbar_wait(&p_full[b], (sidx - 1) & 1);
-                tc_fence_after();
-                if (leader) {
-                    const uint32_t id1 = idesc_bf16(128, nl, false, false);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk)
-                        mma_bf16(tmem + b * 128, desc(lo + ((AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
-                                 desc(lo + ((AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)), id1,
-                                 kk > 0);
-                    mma_commit(&s_full[b]);
-                }
-                __syncwarp();
-                // MMA2 once the softmax wrote P^T (and D2 buffer b was drained by item it-2's epilogue,
-                // which the softmax threads finish before arriving on p_full)
-                mbar_wait(&p_full[b], sidx & 1);
-                tc_fence_after();
-                if (leader && lexp) {   // L export: no alpha_R product (and no o_full: nobody drains D2)
-                    mma_commit(&ld_empty[b]);
-                    if (lc < nlc - 1) mma_commit(&p_empty[b]);   // waited by the item's next step only
-                } else if (leader) {
-                    for (int kk = 0; kk < nl / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
-                        mma_bf16(tmem + 256 + b * 128,
-                                 desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
-                                 desc(lo + ((AlphaSmem::kQc + kk * 2048) >> 4) + (16384u >> 4 << 16)), id2,
-                                 lc > 0 || kk > 0);
-                    if (lc == nlc - 1) mma_commit(&o_full[b]);
-                    mma_commit(&ld_empty[b]);
-                    if (lc < nlc - 1) mma_commit(&p_empty[b]);
-                }
-                __syncwarp();
+            const int sidx = (it >> 1) * nlc + lc;
+            const int nl = step_l(lc);
+            mbar_wait(&p_full[b], sidx & 1);
+            tc_fence_after();
+            if (leader && lexp) {   // L export: no alpha_R product (and no o_full: nobody drains D2)
+                mma_commit(&ld_empty[b]);
+                if (lc < nlc - 1) mma_commit(&p_empty[b]);   // waited by the item's next step only
+            } else if (leader) {
+                for (int kk = 0; kk < nl / 16; ++kk)   // K = l: A = P^T (K-major, 64-l chunks 16 KB apart)
+                    mma_bf16(tmem + 256 + b * 128,
+                             desc(lo + ((AlphaSmem::kP + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                             desc(lo + ((AlphaSmem::kQc + kk * 2048) >> 4) + (16384u >> 4 << 16)), id2,
+                             lc > 0 || kk > 0);
+                if (lc == nlc - 1) mma_commit(&o_full[b]);
+                mma_commit(&ld_empty[b]);
+                if (lc < nlc - 1) mma_commit(&p_empty[b]);
             }
+            __syncwarp();
+        };
+        // MMA1 of step q is issued before MMA2 of step q-1 (software pipeline over the step
+        // order), unless both use the same buffer: its next Q load waits for that MMA2
+        int pit = -1, plc = 0;
+        for (int q = 0; q < nsteps; ++q) {
+            int it, lc;
+            seq(q, it, lc);
+            const int b = it & 1;
+            if (pit >= 0 && (!MBX_ALPHA_IL || (pit & 1) == b)) {
+                mma2(pit, plc);
+                pit = -1;
+            }
+            const uint32_t lo = base_lo + (uint32_t)b * (AlphaSmem::kBuf >> 4);
+            const int sidx = (it >> 1) * nlc + lc;
+            const int nl = step_l(lc);
+            // wait for this step's loads and a free S^T buffer b (the softmax read the previous
+            // step's S^T: p_full precedes it); the pending MMA2 goes first if its P^T is ready
+            // meanwhile, so the next load into its buffer never waits behind this step's loads
+            for (;;) {
+                if (pit >= 0 && mbar_test_uniform(&p_full[pit & 1], ((((pit >> 1) * nlc) + plc) & 1))) {
+                    mma2(pit, plc);
+                    pit = -1;
+                }
+                if (mbar_test_uniform(&ld_full[b], sidx & 1) &&
+                    (sidx < 1 || mbar_test_uniform(&p_full[b], (sidx - 1) & 1)))
+                    break;
+            }
+            tc_fence_after();
+            if (leader) {
+                const uint32_t id1 = idesc_bf16(128, nl, false, false);
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    mma_bf16(tmem + b * 128, desc(lo + ((AlphaSmem::kA + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)),
+                             desc(lo + ((AlphaSmem::kQc + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4) + (1u << 16)), id1,
+                             kk > 0);
+                mma_commit(&s_full[b]);
+            }
+            __syncwarp();
+            if (pit >= 0) mma2(pit, plc);
+            pit = it;
+            plc = lc;
         }
+        if (pit >= 0) mma2(pit, plc);
     } else if (warp < kAlphaThreads / 32) {
         // ------------------------------------------ softmax (thread = key) + epilogue
         const int quad = warp & 3;
