@@ -191,7 +191,9 @@ int mbx_profile_collect_ex(float* start_ms, float* ms, const char** names, int m
 /*
  * Process-wide diagnostic options (initialised from the environment variables
  * of the same name on first use): "MBX_PDL" (programmatic dependent launch,
- * default 1), "MBX_L2HINT" (L2 residency hints, 1), "MBX_PAIR" (row-stage
+ * default 1), "MBX_L2HINT" (L2 residency hints: bit 0 W stores evict_last, bit 1
+ * the W exchange's last reads evict_first; default -1 = bit 1, plus bit 0 when a
+ * launch's exchange exceeds 128 MiB), "MBX_PAIR" (row-stage
  * variant, -1 auto / 0 classic / 1 half-packed), "MBX_WIDE" (wide column stage
  * for s1 <= 32, 0), "MBX_SPLIT" (concurrent halves, -1 auto / 0 / 1),
  * "MBX_DBG" (timing bits, results wrong), "MBX_VERBOSE", "MBX_WAVE" ((b,h)

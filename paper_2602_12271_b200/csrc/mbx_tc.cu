@@ -89,7 +89,7 @@ struct TcParams {
     __nv_bfloat16* out;                   // output base (wide stage's partial-warp stores)
     int64_t out_bh_stride, out_tok_stride;
     int dbg;                              // MBX_DBG bit mask: timing experiments only (wrong results)
-    int l2hint;                           // W stores evict_last, last reads evict_first (MBX_L2HINT=0: off)
+    int l2hint;                           // bit 0: W stores evict_last, bit 1: W last reads evict_first; -1 auto
     CUtensorMap tq128, tk128, tv128;      // flash row stage (s2 > 64): 128-row boxes of q / k / v
     CUtensorMap tar_ld128;                // flash row stage, T >= 2: 128 hat_alpha_R rows of one key
     float* rfac;                          // optional R' export (fp32, factors.py:57-79 layout), last row stage
@@ -282,7 +282,7 @@ static void init_options() {
         return e && e[0] ? atoi(e) : dflt;
     };
     g_opts.pdl = env("MBX_PDL", 1);
-    g_opts.l2hint = env("MBX_L2HINT", 1);
+    g_opts.l2hint = env("MBX_L2HINT", -1);
     g_opts.dbg = env("MBX_DBG", 0);
     g_opts.pair = env("MBX_PAIR", -1);
     g_opts.wide = env("MBX_WIDE", 0);
@@ -409,7 +409,12 @@ static cudaError_t build_plan(const Geometry& g0, const void* q, const void* k, 
     TcParams& P = T->P;
     memset(&P, 0, sizeof(P));
     P.dbg = o.dbg;
-    P.l2hint = o.l2hint;
+    // L2 policy of the W exchange: its last reads evict_first; its stores evict_last only when
+    // the launch's W exceeds L2 (a W that fits stays resident anyway, and marking it evict_last
+    // costs the row stage's K/V reuse: C2, 86 MB, 58.0 -> 56.5 us without it; KV21 halves,
+    // 302 MB each, 280 -> 277 us with it; profiles/r2h_l2hint_ab.txt)
+    const size_t w_bytes = (size_t)g.bh * g.gq * g.s1 * g.gk * g.s2 * 512;
+    P.l2hint = o.l2hint >= 0 ? o.l2hint : 2 | (w_bytes > ((size_t)128 << 20) ? 1 : 0);
     P.rfac = r_factor;
     P.lfac = l_factor;
     const bool flash = g.s2 > kMaxS2;   // long tile rows: online-softmax row stage

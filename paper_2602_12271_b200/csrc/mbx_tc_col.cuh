@@ -131,7 +131,7 @@ __device__ __forceinline__ void col_role(uint8_t* smem, const TcParams& P, const
         const bool leader = elect_one();
         int slot = 0, sph = 0;   // ring position of use n: n % kRing and (n / kRing) & 1
         // the final pass is W's last reader: stream it through L2 without displacing the rest
-        const uint64_t w_policy = P.l2hint && mode == 0 ? l2_evict_first() : l2_evict_normal();
+        const uint64_t w_policy = (P.l2hint & 2) && mode == 0 ? l2_evict_first() : l2_evict_normal();
         int ti = 0;
         auto next_slot = [&]() {
             if (++slot == kRing) {

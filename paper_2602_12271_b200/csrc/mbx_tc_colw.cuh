@@ -104,7 +104,7 @@ tc_column_wide(const __grid_constant__ TcParams P, Geometry g, int mode) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
         // the final pass is W's last reader: stream it through L2 without displacing the rest
-        const uint64_t w_policy = P.l2hint && mode == 0 ? l2_evict_first() : l2_evict_normal();
+        const uint64_t w_policy = (P.l2hint & 2) && mode == 0 ? l2_evict_first() : l2_evict_normal();
         uint32_t n = 0;   // ring uses
         auto load_part = [&](int uu, int part) {
             int col, mt;

@@ -143,7 +143,7 @@ tc_column_wide2(const __grid_constant__ TcParams P, Geometry g) {
       if (warp == 0) {
         // ------------------------------------------ TMA producer (whole warp, elected lane issues)
         const bool leader = elect_one();
-        const uint64_t w_policy = P.l2hint && outm ? l2_evict_first() : l2_evict_normal();   // W's last reader
+        const uint64_t w_policy = (P.l2hint & 2) && outm ? l2_evict_first() : l2_evict_normal();   // W's last reader
         uint32_t n = 0;   // ring uses
         bool waited = false;
         schedule([&](bool is_o, int k) {

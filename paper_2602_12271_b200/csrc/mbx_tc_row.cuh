@@ -511,7 +511,7 @@ __device__ __forceinline__ void row_role(uint8_t* smem, const TcParams& P, const
         // ------------------------------------------------------ epilogue: TMEM -> smem -> TMA store
         const int set = warp >= 10 ? 1 : 0;   // warps 6-9: O_aL, 10-13: O_Y
         // the column stage reads W right after this launch: keep it in L2 ahead of q / k / v
-        const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
+        const uint64_t w_policy = (P.l2hint & 1) ? l2_evict_last() : l2_evict_normal();
         if (set == 1 && !want_y) cur.valid = false;   // no Y this refinement
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;

@@ -332,7 +332,7 @@ tc_row_flash(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wa
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
+        const uint64_t w_policy = (P.l2hint & 1) ? l2_evict_last() : l2_evict_normal();
         __nv_bfloat16* W = const_cast<__nv_bfloat16*>(P.w);
         const uint32_t stg = smem_u32(smem + RowFSmem::kStage + quad * 4096);
         const int64_t rstride = (int64_t)4 * g.nkeys * 64;   // bf16 elements between rows j, j + 1

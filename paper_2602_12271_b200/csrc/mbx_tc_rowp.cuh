@@ -416,7 +416,7 @@ tc_row_pair(const __grid_constant__ TcParams P, Geometry g, int amode_i, int wan
         const int set = warp >= kPairEpi + 4 ? 1 : 0;
         if (set == 1 && !want_y) cur.valid = false;
         // the column stage reads W right after this launch: keep it in L2 ahead of q / k / v
-        const uint64_t w_policy = P.l2hint ? l2_evict_last() : l2_evict_normal();
+        const uint64_t w_policy = (P.l2hint & 1) ? l2_evict_last() : l2_evict_normal();
         const int quad = warp & 3;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const uint32_t obuf = tmem + (set ? kPOY : kPOA) + lane_off;
