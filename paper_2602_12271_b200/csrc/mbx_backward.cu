@@ -22,6 +22,8 @@
 #include <cublas_v2.h>
 #include <dlfcn.h>
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 #include <mutex>
 
 namespace mbx {
@@ -31,6 +33,22 @@ __device__ __forceinline__ float ld(const float* p) { return *p; }
 __device__ __forceinline__ float ld(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ void store(float* p, float x) { *p = x; }
 __device__ __forceinline__ void store(__nv_bfloat16* p, float x) { *p = __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void store4(float* p, float4 x) { *reinterpret_cast<float4*>(p) = x; }
+__device__ __forceinline__ void store4(__nv_bfloat16* p, float4 x) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(x.x, x.y), b = __floats2bfloat162_rn(x.z, x.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+}
 
 // ---------------------------------------------------------------- batched GEMM
 // C[b][m][n] = alpha * sum_{k1 < K1, k2 < K2} A[b][m][k1][k2] B[b][k1][k2][n] (+ C if acc),
@@ -132,6 +150,213 @@ __global__ void __launch_bounds__(kGemmThreads) gemm_batched(Gemm G) {
             *c = G.acc ? *c + v : v;
         }
     }
+}
+
+// ------------------------------------------- batched GEMM on the tensor cores (TF32)
+// The same contraction for bf16 I/O: 64 x 64 CTA tiles, four warps of 32 x 32 issuing
+// mma.sync m16n8k8 TF32 (fp32 accumulate), K in steps of 32 with the next step's
+// global loads in registers while the current one computes.  Each operand is staged
+// in the shared layout its global unit stride gives coalesced loads for: [row][k]
+// (stride 36) when k is the unit stride, [k][row] (stride 72) when rows are -- both
+// bank-conflict free for the stores and for the fragment reads.  The reduction runs
+// k1 outer (K1 > 1 only when it does not fold into one stride), k2 inner.  The
+// per-batch matrices are tiny (30-128 rows), so one launch holds thousands of CTAs and
+// several are resident per SM; cuBLAS's batched TF32 GEMM on these shapes ran at
+// ~1/15 of the bandwidth its bytes need (bwd_dl: 183 us for 77 MB at C2).
+constexpr int kMT = 64, kMK = 32, kMThreads = 128;
+
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// stage a kMT x kMK tile of rows [r0, r0 + kMT) and k2 [k0, k0 + kMK) of operand P into
+// registers.  Element r of a thread: KC -- row tid / 32 + 4 r, k tid % 32 (a warp reads 128 B
+// of one row); else -- row tid % 64, k tid / 64 + 2 r.  One index is fixed per thread, so
+// the address steps by a constant.
+template <bool KC>
+__device__ __forceinline__ void mma_load(float (&x)[kMT * kMK / kMThreads], const float* P, int64_t s_row,
+                                         int64_t s_k, int r0, int rows, int k0, int K2, int tid) {
+    constexpr int kN = kMT * kMK / kMThreads;
+    if (KC) {
+        const int row = r0 + tid / kMK, kk = k0 + tid % kMK;
+        const float* p = P + (int64_t)row * s_row + (int64_t)kk * s_k;
+        const int64_t step = (int64_t)(kMThreads / kMK) * s_row;
+        const bool kin = kk < K2;
+#pragma unroll
+        for (int r = 0; r < kN; ++r, p += step) x[r] = (kin && row + (kMThreads / kMK) * r < rows) ? __ldg(p) : 0.f;
+    } else {
+        const int row = r0 + tid % kMT, kk = k0 + tid / kMT;
+        const float* p = P + (int64_t)row * s_row + (int64_t)kk * s_k;
+        const int64_t step = (int64_t)(kMThreads / kMT) * s_k;
+        const bool rin = row < rows;
+#pragma unroll
+        for (int r = 0; r < kN; ++r, p += step) x[r] = (rin && kk + (kMThreads / kMT) * r < K2) ? __ldg(p) : 0.f;
+    }
+}
+template <bool KC>
+__device__ __forceinline__ void mma_store(float* S, const float (&x)[kMT * kMK / kMThreads], int tid) {
+    constexpr int kN = kMT * kMK / kMThreads;
+    float* s = KC ? S + (tid / kMK) * (kMK + 4) + tid % kMK : S + (tid / kMT) * (kMT + 8) + tid % kMT;
+#pragma unroll
+    for (int r = 0; r < kN; ++r)
+        s[KC ? r * (kMThreads / kMK) * (kMK + 4) : r * (kMThreads / kMT) * (kMT + 8)] = to_tf32(x[r]);
+}
+template <bool KC>
+__device__ __forceinline__ float mma_at(const float* S, int row, int kk) {
+    return S[KC ? row * (kMK + 4) + kk : kk * (kMT + 8) + row];
+}
+// four 8 x 4 (32-bit) matrices of a [row][k] tile: lane L addresses row base_row(L) of matrix L / 8
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const float* p) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+
+template <bool AK, bool BK>
+__global__ void __launch_bounds__(kMThreads) gemm_batched_tf32(Gemm G) {
+    constexpr int kTile = kMT * (kMK + 8);   // >= both layouts (64 x 36, 32 x 72)
+    __shared__ __align__(16) float As[kTile];
+    __shared__ __align__(16) float Bs[kTile];
+    const int tiles_n = (G.N + kMT - 1) / kMT;
+    int64_t bx = blockIdx.x;
+    const int tn = (int)(bx % tiles_n);
+    bx /= tiles_n;
+    int bi[4];
+    bi[3] = (int)(bx % G.nb[3]); bx /= G.nb[3];
+    bi[2] = (int)(bx % G.nb[2]); bx /= G.nb[2];
+    bi[1] = (int)(bx % G.nb[1]); bx /= G.nb[1];
+    bi[0] = (int)bx;
+    const int m0 = blockIdx.y * kMT, n0 = tn * kMT;
+    const float* A = G.A.p;
+    const float* B = G.B.p;
+    float* C = const_cast<float*>(G.C.p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        A += bi[i] * G.A.b[i];
+        B += bi[i] * G.B.b[i];
+        C += bi[i] * G.C.b[i];
+    }
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    float acc[2][4][4] = {};
+    float ra[kMT * kMK / kMThreads], rb[kMT * kMK / kMThreads];
+    const int ksteps = (G.K2 + kMK - 1) / kMK, total = G.K1 * ksteps;
+    mma_load<AK>(ra, A, G.A.s0, G.A.s2, m0, G.M, 0, G.K2, tid);
+    mma_load<BK>(rb, B, G.B.s0, G.B.s2, n0, G.N, 0, G.K2, tid);
+    for (int s = 0; s < total; ++s) {
+        mma_store<AK>(As, ra, tid);
+        mma_store<BK>(Bs, rb, tid);
+        __syncthreads();
+        if (s + 1 < total) {   // next step's loads in flight while this one computes
+            const int k1 = (s + 1) / ksteps, k0 = ((s + 1) - k1 * ksteps) * kMK;
+            mma_load<AK>(ra, A + (int64_t)k1 * G.A.s1, G.A.s0, G.A.s2, m0, G.M, k0, G.K2, tid);
+            mma_load<BK>(rb, B + (int64_t)k1 * G.B.s1, G.B.s0, G.B.s2, n0, G.N, k0, G.K2, tid);
+        }
+#pragma unroll
+        for (int kb = 0; kb < kMK; kb += 8) {
+            uint32_t af[2][4], bf[4][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int m = wm + 16 * i + g;
+                if (AK) {   // matrices (rows 0-7 | 8-15) x (k 0-3 | 4-7) -> a0..a3
+                    const int q = lane >> 3;
+                    ldsm_x4(af[i], As + (wm + 16 * i + (lane & 7) + 8 * (q & 1)) * (kMK + 4) + kb + 4 * (q >> 1));
+                } else {
+                    af[i][0] = __float_as_uint(mma_at<AK>(As, m, kb + t));
+                    af[i][1] = __float_as_uint(mma_at<AK>(As, m + 8, kb + t));
+                    af[i][2] = __float_as_uint(mma_at<AK>(As, m, kb + t + 4));
+                    af[i][3] = __float_as_uint(mma_at<AK>(As, m + 8, kb + t + 4));
+                }
+            }
+            if (BK) {   // matrices (n block j | j + 1) x (k 0-3 | 4-7) -> b0, b1 of j, j + 1
+#pragma unroll
+                for (int j = 0; j < 4; j += 2) {
+                    const int q = lane >> 3;
+                    uint32_t r[4];
+                    ldsm_x4(r, Bs + (wn + 8 * (j + (q >> 1)) + (lane & 7)) * (kMK + 4) + kb + 4 * (q & 1));
+                    bf[j][0] = r[0];
+                    bf[j][1] = r[1];
+                    bf[j + 1][0] = r[2];
+                    bf[j + 1][1] = r[3];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int n = wn + 8 * j + g;
+                    bf[j][0] = __float_as_uint(mma_at<BK>(Bs, n, kb + t));
+                    bf[j][1] = __float_as_uint(mma_at<BK>(Bs, n, kb + t + 4));
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    asm volatile(
+                        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+                        "{%8,%9}, {%0,%1,%2,%3};"
+                        : "+f"(acc[i][j][0]), "+f"(acc[i][j][1]), "+f"(acc[i][j][2]), "+f"(acc[i][j][3])
+                        : "r"(af[i][0]), "r"(af[i][1]), "r"(af[i][2]), "r"(af[i][3]), "r"(bf[j][0]),
+                          "r"(bf[j][1]));
+        }
+        __syncthreads();
+    }
+    // accumulate: every previous C value is loaded before the first store (a read-modify-write
+    // per element would serialise 32 round trips, the stores possibly aliasing later loads)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int m = m0 + wm + 16 * i + g + 8 * h, n = n0 + wn + 8 * j + 2 * t + e;
+                    float& a = acc[i][j][2 * h + e];
+                    a *= G.alpha;
+                    if (G.acc && m < G.M && n < G.N) a += __ldg(C + (int64_t)m * G.C.s0 + (int64_t)n * G.C.s1);
+                }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int m = m0 + wm + 16 * i + g + 8 * h;
+            if (m >= G.M) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int n = n0 + wn + 8 * j + 2 * t + e;
+                    if (n < G.N) C[(int64_t)m * G.C.s0 + (int64_t)n * G.C.s1] = acc[i][j][2 * h + e];
+                }
+        }
+}
+
+// launch of the TF32 kernel: the reduction folded to one k stride when (k1, k2) allow it
+bool gemm_mma(Gemm G, cudaStream_t st) {
+    auto fold = [&](const Operand& o) { return G.K1 == 1 || o.s1 == (int64_t)G.K2 * o.s2; };
+    if (G.K1 > 1 && G.K2 == 1) {   // k1 alone: it becomes the k2 index
+        G.A.s2 = G.A.s1;
+        G.B.s2 = G.B.s1;
+        G.K2 = G.K1;
+        G.K1 = 1;
+    } else if (G.K1 > 1 && fold(G.A) && fold(G.B)) {
+        G.K2 *= G.K1;
+        G.K1 = 1;
+    }
+    const int64_t batches = (int64_t)G.nb[0] * G.nb[1] * G.nb[2] * G.nb[3];
+    const int64_t gx = batches * ((G.N + kMT - 1) / kMT);
+    if (gx > INT32_MAX) return false;
+    dim3 grid((unsigned)gx, (unsigned)((G.M + kMT - 1) / kMT));
+    const bool ak = G.A.s2 == 1 || G.A.s0 != 1, bk = G.B.s2 == 1 || G.B.s0 != 1;
+    if (ak && bk) gemm_batched_tf32<true, true><<<grid, kMThreads, 0, st>>>(G);
+    else if (ak) gemm_batched_tf32<true, false><<<grid, kMThreads, 0, st>>>(G);
+    else if (bk) gemm_batched_tf32<false, true><<<grid, kMThreads, 0, st>>>(G);
+    else gemm_batched_tf32<false, false><<<grid, kMThreads, 0, st>>>(G);
+    return true;
 }
 
 // ---------------------------------------------------------------- row kernels
@@ -237,36 +462,59 @@ __device__ __forceinline__ int64_t slot_row(const Geometry& g, const int32_t* or
     return order ? (int64_t)order[p] : p;
 }
 
-// dst[bh][tile][r][j][e] = scale * src[b, h, row(tile, r, j), e]
+// dst[bh][tile][r][j][e] = scale * src[b, h, row(tile, r, j), e]: one warp per slot row
+// (the row's token index and source offset computed once, lanes over e)
 template <typename T>
 __global__ void gather_tiles(const Geometry g, const T* __restrict__ src, const int64_t* st, const int32_t* order,
                              int tiles, int width, float scale, float* __restrict__ dst) {
-    const int64_t n = (int64_t)g.bh * tiles * g.s1 * g.s2 * width;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int e = (int)(t % width);
-        int64_t x = t / width;
+    const int64_t rows = (int64_t)g.bh * tiles * g.s1 * g.s2;
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t x = w;
         const int j = (int)(x % g.s2); x /= g.s2;
         const int r = (int)(x % g.s1); x /= g.s1;
         const int tile = (int)(x % tiles);
         const int bh = (int)(x / tiles);
         const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
-        dst[t] = scale * ld(src + b * st[0] + h * st[1] + slot_row(g, order, tile, r, j) * st[2] + e);
+        const T* sp = src + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
+        float* dp = dst + w * width;
+        if (width % 128 == 0 && ((uintptr_t)sp % (4 * sizeof(T))) == 0) {   // 4 elements per lane
+            for (int e = 4 * lane; e < width; e += 128) {
+                float4 x = ld4(sp + e);
+                store4(dp + e, make_float4(scale * x.x, scale * x.y, scale * x.z, scale * x.w));
+            }
+        } else {
+            for (int e = lane; e < width; e += 32) dp[e] = scale * ld(sp + e);
+        }
     }
 }
 
 template <typename T>
 __global__ void scatter_tiles(const Geometry g, const float* __restrict__ src, const int64_t* st, const int32_t* order,
                               int tiles, int width, float scale, T* __restrict__ dst) {
-    const int64_t n = (int64_t)g.bh * tiles * g.s1 * g.s2 * width;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-        const int e = (int)(t % width);
-        int64_t x = t / width;
+    const int64_t rows = (int64_t)g.bh * tiles * g.s1 * g.s2;
+    const int lane = threadIdx.x & 31;
+    const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
+    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t x = w;
         const int j = (int)(x % g.s2); x /= g.s2;
         const int r = (int)(x % g.s1); x /= g.s1;
         const int tile = (int)(x % tiles);
         const int bh = (int)(x / tiles);
         const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
-        store(dst + b * st[0] + h * st[1] + slot_row(g, order, tile, r, j) * st[2] + e, scale * src[t]);
+        T* dp = dst + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
+        const float* sp = src + w * width;
+        if (width % 128 == 0 && ((uintptr_t)dp % (4 * sizeof(T))) == 0) {
+            for (int e = 4 * lane; e < width; e += 128) {
+                float4 x = ld4(sp + e);
+                store4(dp + e, make_float4(scale * x.x, scale * x.y, scale * x.z, scale * x.w));
+            }
+        } else {
+            for (int e = lane; e < width; e += 32) store(dp + e, scale * sp[e]);
+        }
     }
 }
 
@@ -467,9 +715,24 @@ void gemm(Ctx& c, const char* name, int M, int N, int K1, int K2, const int nb[4
     G.acc = acc;
     const int64_t batches = (int64_t)nb[0] * nb[1] * nb[2] * nb[3];
     ProfScope p(name, c.st);
-    if (c.tf32 && gemm_tf32(G, c.ptrs, c.max_batches, c.st)) {
-        c.err = cudaGetLastError();
-        return;
+    // bf16 I/O: the in-library TF32 kernel, except for the contractions where cuBLAS's
+    // batched TF32 GEMM measured faster at C2 (scripts/bwd_profile.py, profiles/r2k_*):
+    // the two with row-contiguous operands on both sides (the kernel's scalar fragment
+    // reads) and the three s2 x s2 outputs reduced over d.  MBX_BWD_CUBLAS overrides the
+    // list ("all", "none", or comma-separated names; A/B only).
+    static const char* cublas_names = [] {
+        const char* e = getenv("MBX_BWD_CUBLAS");
+        return e ? e : "bwd_dalpha_l,bwd_dy,bwd_dr_k,bwd_dr_v,bwd_z";
+    }();
+    if (c.tf32) {
+        bool prefer_cublas = strcmp(cublas_names, "all") == 0;
+        for (const char* p = cublas_names; !prefer_cublas && (p = strstr(p, name)) != nullptr; ++p)
+            prefer_cublas = (p == cublas_names || p[-1] == ',') && (p[strlen(name)] == ',' || !p[strlen(name)]);
+        if ((prefer_cublas && gemm_tf32(G, c.ptrs, c.max_batches, c.st)) || gemm_mma(G, c.st) ||
+            gemm_tf32(G, c.ptrs, c.max_batches, c.st)) {
+            c.err = cudaGetLastError();
+            return;
+        }
     }
     dim3 grid((unsigned)(batches * ((N + kTN - 1) / kTN)), (unsigned)((M + kTM - 1) / kTM));
     gemm_batched<<<grid, kGemmThreads, 0, c.st>>>(G);
@@ -506,10 +769,14 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
         if (e != cudaSuccess) return e;
     }
     const unsigned gb = 148 * 8;
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, k, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, b.Kt);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, v, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, b.Vt);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, dout, dstr + 9, g.q_order, (int)gq, (int)dv, 1.f, b.dOt);
+    { ProfScope ps_("bwd_gather", stream);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt); }
+    { ProfScope ps_("bwd_gather", stream);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, k, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, b.Kt); }
+    { ProfScope ps_("bwd_gather", stream);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, v, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, b.Vt); }
+    { ProfScope ps_("bwd_gather", stream);
+    gather_tiles<T><<<gb, 256, 0, stream>>>(g, dout, dstr + 9, g.q_order, (int)gq, (int)dv, 1.f, b.dOt); }
     cudaMemsetAsync(b.dQt, 0, sizeof(float) * bh * tq * d, stream);
     cudaMemsetAsync(b.dKt, 0, sizeof(float) * bh * tk * d, stream);
     cudaMemsetAsync(b.dVt, 0, sizeof(float) * bh * tk * dv, stream);
@@ -543,7 +810,8 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
             gemm(c, "bwd_alpha_r", (int)s1, (int)d, 1, (int)s1, nb_acj,
                  op(Lp, 1, 0, s1, gq * l_a, l_a, l_c, l_j), op(b.Qt, 1, 0, s2 * d, gq * qt_a, qt_a, 0, d),
                  op(b.Ah, pd_k, 1, 0, gq * pd_a, pd_a, pd_c, d), 1.f, 0);
-            sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(Lp, b.cR, bh * pairs, (int)s2, (int)s1, 1.f);
+            { ProfScope ps_("bwd_sum_l", stream);
+            sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(Lp, b.cR, bh * pairs, (int)s2, (int)s1, 1.f); }
             normalize_rows<<<blocks_for(bh * pairs * d), 256, 0, stream>>>(b.Ah, b.cR, bh * pairs * d, (int)d,
                                                                           g.eps_div);
             At = b.Ah;
@@ -561,8 +829,9 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
                  op(b.Y, pv_k, 0, 1, gq * pv_a, pv_a, pv_c, dv), op(b.dL, s1, 1, 0, gq * l_a, l_a, l_c, l_j), 1.f, 0);
         }
         // dS = L (dL - sum L dL)
+        { ProfScope ps_("bwd_softmax_cols", stream);
         softmax_bwd_cols<<<blocks_for(bha * s2 * s1 * 32), 256, 0, stream>>>(L, b.dL, bha * s2 * s1, (int)gk, (int)s2,
-                                                                          (int)s1);
+                                                                          (int)s1); }
         // dQ[a][l][j][:] += sum_(c,k) dS[a][c][j][l][k] aL[a][c][k][j][:]   (M = l, N = e, K = (c, k))
         gemm(c, "bwd_dq_col", (int)s1, (int)d, (int)gk, (int)s1, nb_aj, op(b.dL, s1, l_c, 1, gq * l_a, l_a, 0, l_j),
              op(b.aL, 1, pd_c, pd_k, gq * pd_a, pd_a, 0, d), op(b.dQt, s2 * d, 1, 0, gq * qt_a, qt_a, 0, d), 1.f, 1);
@@ -570,7 +839,8 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
         gemm(c, "bwd_dalpha_l", (int)s1, (int)d, 1, (int)s1, nb_acj, op(b.dL, 1, 0, s1, gq * l_a, l_a, l_c, l_j),
              op(b.Qt, 1, 0, s2 * d, gq * qt_a, qt_a, 0, d), op(b.daL, pd_k, 1, 0, gq * pd_a, pd_a, pd_c, d), 1.f, 0);
         // dc_L[a][c][k][j] = -sum_l dS
-        sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(b.dL, b.dcL, bh * pairs, (int)s2, (int)s1, -1.f);
+        { ProfScope ps_("bwd_sum_l", stream);
+        sum_over_l<<<blocks_for(bh * pairs), 256, 0, stream>>>(b.dL, b.dcL, bh * pairs, (int)s2, (int)s1, -1.f); }
         if (last) {
             // dY[a][c][k][j][:] = sum_l L[a][c][j][l][k] dO[a][l][j][:]
             gemm(c, "bwd_dy", (int)s1, (int)dv, 1, (int)s1, nb_acj, op(L, 1, 0, s1, gq * l_a, l_a, l_c, l_j),
@@ -587,7 +857,8 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
         gemm(c, "bwd_dr_k", (int)s2, (int)s2, 1, (int)d, nb_ack, op(b.daL, d, 0, 1, gq * pd_a, pd_a, pd_c, pd_k),
              op(b.Kt, d, 0, 1, gk * kt_c, 0, kt_c, s2 * d), op(b.dR, s2, 1, 0, gq * r_a, r_a, r_c, r_k), 1.f, last);
         // dz (in place over dR)
-        softmax_bwd_rows<<<blocks_for(bh * pairs * 32), 256, 0, stream>>>(R, b.z, b.dR, b.dcL, bh * pairs, (int)s2);
+        { ProfScope ps_("bwd_softmax_rows", stream);
+        softmax_bwd_rows<<<blocks_for(bh * pairs * 32), 256, 0, stream>>>(R, b.z, b.dR, b.dcL, bh * pairs, (int)s2); }
         // dK[c][k][i][:] += sum_(a,j) dz[a][c][k][j][i] A_t[a][c][k][j][:] + R daL   (M = i, N = e, K = (a, j))
         {
             Operand Ab = At_rows;   // as B[k1 = a][k2 = j][n = e]
@@ -629,9 +900,12 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
         if ((c.err = cudaGetLastError()) != cudaSuccess) return c.err;
     }
     // scatter back to token order: dq = scale * dQt (Q entered the solver as scale * q)
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dQt, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, dq_out);
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dKt, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, dk_out);
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dVt, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, dv_out);
+    { ProfScope ps_("bwd_scatter", stream);
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dQt, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, dq_out); }
+    { ProfScope ps_("bwd_scatter", stream);
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dKt, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, dk_out); }
+    { ProfScope ps_("bwd_scatter", stream);
+    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dVt, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, dv_out); }
     (void)nb_ak;
     return cudaGetLastError();
 }

@@ -147,3 +147,24 @@ def test_backward_head_chunks_equal_one_call(cuda):
     for a, b in zip(full, chunked):
         err = ((a.float() - b.float()).norm() / a.float().norm()).item()
         assert err < 2e-3, err
+
+
+@pytest.mark.parametrize("name,fhw,kind,q_frames,T", CASES, ids=[c[0] for c in CASES])
+def test_backward_bf16_matches_autograd_oracle(cuda, name, fhw, kind, q_frames, T):
+    """bf16 I/O runs the contractions on the tensor cores (TF32 mma.sync batched GEMM):
+    every plan geometry (folded and two-level reduction indices, broadcast operands)
+    within the bf16 tolerance of the fp64 gradients of the bf16-rounded inputs."""
+    shape = pk.VideoShape(*fhw)
+    plan = _plan(shape, kind)
+    low = pk.lower_chunked(plan, q_frames) if q_frames else pk.lower_square(plan)
+    g = torch.Generator(device="cpu").manual_seed(zlib.crc32(name.encode()) % 991)
+    B, H, d = 1, 2, 128
+    q = torch.randn(B, H, low.n_q, d, generator=g).to(cuda, torch.bfloat16)
+    k, v = (torch.randn(B, H, low.n_kv, d, generator=g).to(cuda, torch.bfloat16) for _ in range(2))
+    dout = torch.randn(B, H, low.n_q, d, generator=g).to(cuda, torch.bfloat16)
+    dq, dk, dv = ops.backward(q, k, v, dout, low, T)
+    for h in range(H):
+        rq, rk, rv = _oracle_grads(q, k, v, dout, low, T, 0, h)
+        for got, ref, nm in ((dq, rq, "dq"), (dk, rk, "dk"), (dv, rv, "dv")):
+            err = orc.rel_l2(got[0, h].float().cpu().numpy(), ref.numpy())
+            assert err < BF16_TOL, (name, nm, h, err)
