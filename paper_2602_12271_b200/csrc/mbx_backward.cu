@@ -165,21 +165,39 @@ __global__ void __launch_bounds__(kGemmThreads) gemm_batched(Gemm G) {
 // ~1/15 of the bandwidth its bytes need (bwd_dl: 183 us for 77 MB at C2).
 constexpr int kMT = 64, kMK = 32, kMThreads = 128;
 
-__device__ __forceinline__ float to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return __uint_as_float(r);
-}
 
 // stage a kMT x kMK tile of rows [r0, r0 + kMT) and k2 [k0, k0 + kMK) of operand P into
-// registers.  Element r of a thread: KC -- row tid / 32 + 4 r, k tid % 32 (a warp reads 128 B
-// of one row); else -- row tid % 64, k tid / 64 + 2 r.  One index is fixed per thread, so
-// the address steps by a constant.
-template <bool KC>
+// registers.  MODE bit 0 (KC): k is the unit stride, else rows are; bit 1 (VEC): 16-byte
+// loads along the unit stride (host-checked alignment, extent a multiple of 4).  Scalar
+// KC -- element r of a thread is row tid / 32 + 4 r, k tid % 32 (a warp reads 128 B of one
+// row); scalar rows -- row tid % 64, k tid / 64 + 2 r.  Vector KC -- row tid / 8 + 16 r,
+// k 4 (tid % 8); vector rows -- rows 4 (tid % 16), k tid / 16 + 8 r.  One index is fixed
+// per thread, so the address steps by a constant.
+template <int MODE>
 __device__ __forceinline__ void mma_load(float (&x)[kMT * kMK / kMThreads], const float* P, int64_t s_row,
                                          int64_t s_k, int r0, int rows, int k0, int K2, int tid) {
     constexpr int kN = kMT * kMK / kMThreads;
-    if (KC) {
+    if (MODE == 3) {
+        const int row = r0 + tid / 8, kk = k0 + 4 * (tid % 8);
+        const float* p = P + (int64_t)row * s_row + kk;
+        const bool kin = kk < K2;
+#pragma unroll
+        for (int r = 0; r < kN / 4; ++r) {
+            const float4 v = (kin && row + 16 * r < rows) ? __ldg(reinterpret_cast<const float4*>(p + 16 * r * s_row))
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[4 * r] = v.x; x[4 * r + 1] = v.y; x[4 * r + 2] = v.z; x[4 * r + 3] = v.w;
+        }
+    } else if (MODE == 2) {
+        const int row = r0 + 4 * (tid % 16), kk = k0 + tid / 16;
+        const float* p = P + row + (int64_t)kk * s_k;
+        const bool rin = row < rows;
+#pragma unroll
+        for (int r = 0; r < kN / 4; ++r) {
+            const float4 v = (rin && kk + 8 * r < K2) ? __ldg(reinterpret_cast<const float4*>(p + 8 * r * s_k))
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[4 * r] = v.x; x[4 * r + 1] = v.y; x[4 * r + 2] = v.z; x[4 * r + 3] = v.w;
+        }
+    } else if (MODE == 1) {
         const int row = r0 + tid / kMK, kk = k0 + tid % kMK;
         const float* p = P + (int64_t)row * s_row + (int64_t)kk * s_k;
         const int64_t step = (int64_t)(kMThreads / kMK) * s_row;
@@ -195,13 +213,24 @@ __device__ __forceinline__ void mma_load(float (&x)[kMT * kMK / kMThreads], cons
         for (int r = 0; r < kN; ++r, p += step) x[r] = (rin && kk + (kMThreads / kMT) * r < K2) ? __ldg(p) : 0.f;
     }
 }
-template <bool KC>
+// fp32 -> TF32, round to nearest (ties away): two integer ops instead of the emulated cvt.rna
+__device__ __forceinline__ float tf32r(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u); }
+template <int MODE>
 __device__ __forceinline__ void mma_store(float* S, const float (&x)[kMT * kMK / kMThreads], int tid) {
     constexpr int kN = kMT * kMK / kMThreads;
-    float* s = KC ? S + (tid / kMK) * (kMK + 4) + tid % kMK : S + (tid / kMT) * (kMT + 8) + tid % kMT;
+    if (MODE >= 2) {
+        float* s = MODE == 3 ? S + (tid / 8) * (kMK + 4) + 4 * (tid % 8) : S + (tid / 16) * (kMT + 8) + 4 * (tid % 16);
 #pragma unroll
-    for (int r = 0; r < kN; ++r)
-        s[KC ? r * (kMThreads / kMK) * (kMK + 4) : r * (kMThreads / kMT) * (kMT + 8)] = to_tf32(x[r]);
+        for (int r = 0; r < kN / 4; ++r)
+            *reinterpret_cast<float4*>(s + (MODE == 3 ? 16 * r * (kMK + 4) : 8 * r * (kMT + 8))) =
+                make_float4(tf32r(x[4 * r]), tf32r(x[4 * r + 1]), tf32r(x[4 * r + 2]), tf32r(x[4 * r + 3]));
+    } else {
+        constexpr bool KC = MODE == 1;
+        float* s = KC ? S + (tid / kMK) * (kMK + 4) + tid % kMK : S + (tid / kMT) * (kMT + 8) + tid % kMT;
+#pragma unroll
+        for (int r = 0; r < kN; ++r)
+            s[KC ? r * (kMThreads / kMK) * (kMK + 4) : r * (kMThreads / kMT) * (kMT + 8)] = tf32r(x[r]);
+    }
 }
 template <bool KC>
 __device__ __forceinline__ float mma_at(const float* S, int row, int kk) {
@@ -215,11 +244,45 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const float* p) {
                  : "r"(a));
 }
 
-template <bool AK, bool BK>
+// 16-byte cp.async of a vector-mode tile straight into its shared layout (zero-filled
+// outside [rows) x [K2)); the MMA then reads fp32 bits as TF32 (truncation)
+template <int MODE>
+__device__ __forceinline__ void mma_issue_async(float* S, const float* P, int64_t s_row, int64_t s_k, int r0,
+                                                int rows, int k0, int K2, int tid) {
+#pragma unroll
+    for (int r = 0; r < kMT * kMK / kMThreads / 4; ++r) {
+        int row, kk;
+        const float* src;
+        float* dst;
+        if (MODE == 3) {
+            row = tid / 8 + 16 * r;
+            kk = 4 * (tid % 8);
+            src = P + (int64_t)(r0 + row) * s_row + k0 + kk;
+            dst = S + row * (kMK + 4) + kk;
+        } else {
+            row = 4 * (tid % 16);
+            kk = tid / 16 + 8 * r;
+            src = P + (r0 + row) + (int64_t)(k0 + kk) * s_k;
+            dst = S + kk * (kMT + 8) + row;
+        }
+        const bool ok = r0 + row < rows && k0 + kk < K2;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(ok ? src : P), "r"(ok ? 16 : 0)
+                     : "memory");
+    }
+}
+constexpr int kMStages = 3;
+constexpr int kMTile = kMT * (kMK + 4);   // floats per operand tile, both layouts (64 x 36 = 32 x 72)
+__host__ __device__ constexpr size_t mma_smem_bytes(bool async) {
+    return (async ? kMStages : 1) * 2 * kMTile * sizeof(float);
+}
+
+template <int AM, int BM>
 __global__ void __launch_bounds__(kMThreads) gemm_batched_tf32(Gemm G) {
-    constexpr int kTile = kMT * (kMK + 8);   // >= both layouts (64 x 36, 32 x 72)
-    __shared__ __align__(16) float As[kTile];
-    __shared__ __align__(16) float Bs[kTile];
+    constexpr bool AK = AM & 1, BK = BM & 1;
+    // both operands 16-byte aligned: a kMStages-deep cp.async ring, else registers-staged steps
+    constexpr bool ASYNC = AM >= 2 && BM >= 2;
+    extern __shared__ __align__(16) float mma_smem[];
     const int tiles_n = (G.N + kMT - 1) / kMT;
     int64_t bx = blockIdx.x;
     const int tn = (int)(bx % tiles_n);
@@ -243,18 +306,43 @@ __global__ void __launch_bounds__(kMThreads) gemm_batched_tf32(Gemm G) {
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
     float acc[2][4][4] = {};
-    float ra[kMT * kMK / kMThreads], rb[kMT * kMK / kMThreads];
+    float ra[ASYNC ? 1 : kMT * kMK / kMThreads], rb[ASYNC ? 1 : kMT * kMK / kMThreads];
     const int ksteps = (G.K2 + kMK - 1) / kMK, total = G.K1 * ksteps;
-    mma_load<AK>(ra, A, G.A.s0, G.A.s2, m0, G.M, 0, G.K2, tid);
-    mma_load<BK>(rb, B, G.B.s0, G.B.s2, n0, G.N, 0, G.K2, tid);
+    auto issue = [&](int step) {   // ASYNC: step -> ring slot step % kMStages
+        const int k1 = step / ksteps, k0 = (step - k1 * ksteps) * kMK;
+        float* sa = mma_smem + (step % kMStages) * 2 * kMTile;
+        if constexpr (ASYNC) {
+            mma_issue_async<AM>(sa, A + (int64_t)k1 * G.A.s1, G.A.s0, G.A.s2, m0, G.M, k0, G.K2, tid);
+            mma_issue_async<BM>(sa + kMTile, B + (int64_t)k1 * G.B.s1, G.B.s0, G.B.s2, n0, G.N, k0, G.K2, tid);
+        }
+    };
+    if constexpr (ASYNC) {
+#pragma unroll
+        for (int p = 0; p < kMStages - 1; ++p) {
+            if (p < total) issue(p);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    } else {
+        mma_load<AM>(ra, A, G.A.s0, G.A.s2, m0, G.M, 0, G.K2, tid);
+        mma_load<BM>(rb, B, G.B.s0, G.B.s2, n0, G.N, 0, G.K2, tid);
+    }
     for (int s = 0; s < total; ++s) {
-        mma_store<AK>(As, ra, tid);
-        mma_store<BK>(Bs, rb, tid);
-        __syncthreads();
-        if (s + 1 < total) {   // next step's loads in flight while this one computes
-            const int k1 = (s + 1) / ksteps, k0 = ((s + 1) - k1 * ksteps) * kMK;
-            mma_load<AK>(ra, A + (int64_t)k1 * G.A.s1, G.A.s0, G.A.s2, m0, G.M, k0, G.K2, tid);
-            mma_load<BK>(rb, B + (int64_t)k1 * G.B.s1, G.B.s0, G.B.s2, n0, G.N, k0, G.K2, tid);
+        const float* As = mma_smem + (ASYNC ? (s % kMStages) * 2 * kMTile : 0);
+        const float* Bs = As + kMTile;
+        if constexpr (ASYNC) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kMStages - 2) : "memory");
+            __syncthreads();   // step s landed for every thread; slot (s - 1) % kMStages is free
+            if (s + kMStages - 1 < total) issue(s + kMStages - 1);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        } else {
+            mma_store<AM>(mma_smem, ra, tid);
+            mma_store<BM>(mma_smem + kMTile, rb, tid);
+            __syncthreads();
+            if (s + 1 < total) {   // next step's loads in flight while this one computes
+                const int k1 = (s + 1) / ksteps, k0 = ((s + 1) - k1 * ksteps) * kMK;
+                mma_load<AM>(ra, A + (int64_t)k1 * G.A.s1, G.A.s0, G.A.s2, m0, G.M, k0, G.K2, tid);
+                mma_load<BM>(rb, B + (int64_t)k1 * G.B.s1, G.B.s0, G.B.s2, n0, G.N, k0, G.K2, tid);
+            }
         }
 #pragma unroll
         for (int kb = 0; kb < kMK; kb += 8) {
@@ -302,7 +390,7 @@ __global__ void __launch_bounds__(kMThreads) gemm_batched_tf32(Gemm G) {
                         : "r"(af[i][0]), "r"(af[i][1]), "r"(af[i][2]), "r"(af[i][3]), "r"(bf[j][0]),
                           "r"(bf[j][1]));
         }
-        __syncthreads();
+        if constexpr (!ASYNC) __syncthreads();
     }
     // accumulate: every previous C value is loaded before the first store (a read-modify-write
     // per element would serialise 32 round trips, the stores possibly aliasing later loads)
@@ -351,12 +439,31 @@ bool gemm_mma(Gemm G, cudaStream_t st) {
     const int64_t gx = batches * ((G.N + kMT - 1) / kMT);
     if (gx > INT32_MAX) return false;
     dim3 grid((unsigned)gx, (unsigned)((G.M + kMT - 1) / kMT));
-    const bool ak = G.A.s2 == 1 || G.A.s0 != 1, bk = G.B.s2 == 1 || G.B.s0 != 1;
-    if (ak && bk) gemm_batched_tf32<true, true><<<grid, kMThreads, 0, st>>>(G);
-    else if (ak) gemm_batched_tf32<true, false><<<grid, kMThreads, 0, st>>>(G);
-    else if (bk) gemm_batched_tf32<false, true><<<grid, kMThreads, 0, st>>>(G);
-    else gemm_batched_tf32<false, false><<<grid, kMThreads, 0, st>>>(G);
-    return true;
+    // operand mode: bit 0 k-contiguous staging, bit 1 16-byte loads (every offset a multiple of 4)
+    auto mode = [&](const Operand& o, int rows) {
+        const bool kc = o.s2 == 1 || o.s0 != 1;
+        bool vec = ((uintptr_t)o.p % 16) == 0 && (G.K1 == 1 || o.s1 % 4 == 0);
+        for (int i = 0; i < 4; ++i) vec = vec && o.b[i] % 4 == 0;
+        vec = vec && (kc ? o.s2 == 1 && o.s0 % 4 == 0 && G.K2 % 4 == 0 : o.s0 == 1 && o.s2 % 4 == 0 && rows % 4 == 0);
+        return (kc ? 1 : 0) | (vec ? 2 : 0);
+    };
+    const int am = mode(G.A, G.M), bm = mode(G.B, G.N);
+#define MBX_TF32_CASE(X, Y) \
+    if (am == X && bm == Y) {                                                                          \
+        constexpr size_t smem = mma_smem_bytes(X >= 2 && Y >= 2);                                      \
+        if (smem > 48 * 1024 &&                                                                        \
+            cudaFuncSetAttribute(gemm_batched_tf32<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 (int)smem) != cudaSuccess)                                            \
+            return false;                                                                              \
+        gemm_batched_tf32<X, Y><<<grid, kMThreads, smem, st>>>(G);                                     \
+        return true;                                                                                   \
+    }
+    MBX_TF32_CASE(0, 0) MBX_TF32_CASE(0, 1) MBX_TF32_CASE(0, 2) MBX_TF32_CASE(0, 3)
+    MBX_TF32_CASE(1, 0) MBX_TF32_CASE(1, 1) MBX_TF32_CASE(1, 2) MBX_TF32_CASE(1, 3)
+    MBX_TF32_CASE(2, 0) MBX_TF32_CASE(2, 1) MBX_TF32_CASE(2, 2) MBX_TF32_CASE(2, 3)
+    MBX_TF32_CASE(3, 0) MBX_TF32_CASE(3, 1) MBX_TF32_CASE(3, 2) MBX_TF32_CASE(3, 3)
+#undef MBX_TF32_CASE
+    return false;
 }
 
 // ---------------------------------------------------------------- row kernels
