@@ -711,7 +711,7 @@ def run_ours(args):
                 dense_bwd = f"unavailable: {type(e).__name__}"
         bwd = {"ms": round(bwd_ms, 5), "includes": "forward recompute with factor export + mbx_backward",
                "dense_fwd_plus_bwd_ms_cudnn": dense_bwd,
-               "arith": ("TF32 tensor-core batched GEMMs (cuBLAS) + fp32 softmax-backward kernels" if dtype == torch.bfloat16
+               "arith": ("TF32 tensor-core batched GEMMs (in-library mma.sync kernel; cuBLAS for 5 contractions) + fp32 softmax-backward kernels" if dtype == torch.bfloat16
                          else "fp32 SIMT (batched GEMM chain)"),
                "kernels_ms": {kk: round(vv, 5) for kk, vv in sorted(bk.items(), key=lambda x: -x[1])[:8]}}
 
