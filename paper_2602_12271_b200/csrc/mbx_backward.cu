@@ -271,14 +271,20 @@ __device__ __forceinline__ void mma_issue_async(float* S, const float* P, int64_
                      : "memory");
     }
 }
-constexpr int kMStages = 3;
+#ifndef MBX_BWD_MINB
+#define MBX_BWD_MINB 6
+#endif
+#ifndef MBX_BWD_STAGES
+#define MBX_BWD_STAGES 2
+#endif
+constexpr int kMStages = MBX_BWD_STAGES;
 constexpr int kMTile = kMT * (kMK + 4);   // floats per operand tile, both layouts (64 x 36 = 32 x 72)
 __host__ __device__ constexpr size_t mma_smem_bytes(bool async) {
     return (async ? kMStages : 1) * 2 * kMTile * sizeof(float);
 }
 
 template <int AM, int BM>
-__global__ void __launch_bounds__(kMThreads) gemm_batched_tf32(Gemm G) {
+__global__ void __launch_bounds__(kMThreads, MBX_BWD_MINB) gemm_batched_tf32(Gemm G) {
     constexpr bool AK = AM & 1, BK = BM & 1;
     // both operands 16-byte aligned: a kMStages-deep cp.async ring, else registers-staged steps
     constexpr bool ASYNC = AM >= 2 && BM >= 2;
@@ -515,7 +521,30 @@ __global__ void softmax_bwd_rows(const float* __restrict__ R, const float* __res
     const float* r = R + w * s2;
     const float* zz = z + w * s2;
     float* d = dR + w * s2;
+    const float c = dcl[w];
     float srd = 0.f, srz = 0.f;
+    if (s2 <= 64) {   // the row in registers: one round of loads, no re-read
+        float rv[2], dv[2], zv[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int i = lane + 32 * u;
+            const bool in = i < s2;
+            rv[u] = in ? r[i] : 0.f;
+            dv[u] = in ? d[i] : 0.f;
+            zv[u] = in ? zz[i] : 0.f;
+            srd += rv[u] * dv[u];
+            srz += rv[u] * zv[u];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            srd += __shfl_xor_sync(0xffffffffu, srd, o);
+            srz += __shfl_xor_sync(0xffffffffu, srz, o);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (lane + 32 * u < s2) d[lane + 32 * u] = rv[u] * (dv[u] - srd) + c * rv[u] * (zv[u] - srz);
+        return;
+    }
     for (int i = lane; i < s2; i += 32) {
         srd += r[i] * d[i];
         srz += r[i] * zz[i];
@@ -525,7 +554,6 @@ __global__ void softmax_bwd_rows(const float* __restrict__ R, const float* __res
         srd += __shfl_xor_sync(0xffffffffu, srd, o);
         srz += __shfl_xor_sync(0xffffffffu, srz, o);
     }
-    const float c = dcl[w];
     for (int i = lane; i < s2; i += 32) d[i] = r[i] * (d[i] - srd) + c * r[i] * (zz[i] - srz);
 }
 
@@ -579,11 +607,11 @@ __global__ void gather_tiles(const Geometry g, const T* __restrict__ src, const 
     const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        int64_t x = w;
-        const int j = (int)(x % g.s2); x /= g.s2;
-        const int r = (int)(x % g.s1); x /= g.s1;
-        const int tile = (int)(x % tiles);
-        const int bh = (int)(x / tiles);
+        uint32_t x = (uint32_t)w;   // rows < 2^32 (host-checked)
+        const int j = (int)(x % (uint32_t)g.s2); x /= (uint32_t)g.s2;
+        const int r = (int)(x % (uint32_t)g.s1); x /= (uint32_t)g.s1;
+        const int tile = (int)(x % (uint32_t)tiles);
+        const int bh = (int)(x / (uint32_t)tiles);
         const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
         const T* sp = src + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
         float* dp = dst + w * width;
@@ -606,11 +634,11 @@ __global__ void scatter_tiles(const Geometry g, const float* __restrict__ src, c
     const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        int64_t x = w;
-        const int j = (int)(x % g.s2); x /= g.s2;
-        const int r = (int)(x % g.s1); x /= g.s1;
-        const int tile = (int)(x % tiles);
-        const int bh = (int)(x / tiles);
+        uint32_t x = (uint32_t)w;   // rows < 2^32 (host-checked)
+        const int j = (int)(x % (uint32_t)g.s2); x /= (uint32_t)g.s2;
+        const int r = (int)(x % (uint32_t)g.s1); x /= (uint32_t)g.s1;
+        const int tile = (int)(x % (uint32_t)tiles);
+        const int bh = (int)(x / (uint32_t)tiles);
         const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
         T* dp = dst + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
         const float* sp = src + w * width;
@@ -875,7 +903,10 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
         cudaError_t e = cudaMemcpyAsync(dstr, h, sizeof(h), cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return e;
     }
-    const unsigned gb = 148 * 8;
+    // gathers / scatters: one warp per slot row, all rows resident in one pass
+    const int64_t slot_rows = bh * (gq > gk ? gq : gk) * s1 * s2;
+    if (slot_rows >= (int64_t)UINT32_MAX) return cudaErrorInvalidValue;
+    const unsigned gb = (unsigned)((slot_rows + 7) / 8);
     { ProfScope ps_("bwd_gather", stream);
     gather_tiles<T><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt); }
     { ProfScope ps_("bwd_gather", stream);
