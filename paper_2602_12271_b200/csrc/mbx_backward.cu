@@ -486,6 +486,24 @@ __global__ void softmax_bwd_cols(const float* __restrict__ L, float* __restrict_
     const int64_t base = bha * gk * cst + ((int64_t)j * s1 + l) * s1;
     const int n = gk * s1;
     float D = 0.f;
+    if (n <= 128) {   // the row in registers: one round of loads, no re-read
+        float lv[4], dv[4];
+        int64_t off[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x = lane + 32 * u;
+            off[u] = base + (int64_t)(x / s1) * cst + x % s1;
+            lv[u] = x < n ? L[off[u]] : 0.f;
+            dv[u] = x < n ? dL[off[u]] : 0.f;
+            D += lv[u] * dv[u];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) D += __shfl_xor_sync(0xffffffffu, D, o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (lane + 32 * u < n) dL[off[u]] = lv[u] * (dv[u] - D);
+        return;
+    }
     for (int x = lane; x < n; x += 32) {
         const int64_t o = base + (x / s1) * cst + x % s1;
         D += L[o] * dL[o];

@@ -1,3 +1,3 @@
 mkdir -p gpurun_out/r2l
 rm -f gpurun_out/r2l/*
-timeout 600 ncu --section SpeedOfLight --section Occupancy --section LaunchStats --section MemoryWorkloadAnalysis --clock-control none -k regex:gemm_batched_tf32 -s 13 -c 13 -o gpurun_out/r2l/bwd_mma2 python scripts/bwd_profile.py > gpurun_out/r2l/ncu.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:gemm_batched_tf32 -s 2 -c 1 -o gpurun_out/r2l/bwd_dl python scripts/bwd_profile.py 1 > gpurun_out/r2l/ncu.log 2>&1
