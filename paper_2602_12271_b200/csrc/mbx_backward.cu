@@ -521,12 +521,13 @@ __global__ void sum_over_l(const float* __restrict__ X, float* __restrict__ out,
                            float sign) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    const int j = (int)(t % s2), k = (int)((t / s2) % s1);
+    // k fastest across threads: each step over l reads consecutive k (coalesced)
+    const int k = (int)(t % s1), j = (int)((t / s1) % s2);
     const int64_t bhac = t / ((int64_t)s2 * s1);
     const float* x = X + (bhac * s2 + j) * s1 * s1 + k;
     float s = 0.f;
     for (int l = 0; l < s1; ++l) s += x[(int64_t)l * s1];
-    out[t] = sign * s;
+    out[(bhac * s1 + k) * s2 + j] = sign * s;
 }
 
 // Row softmax backward of the row stage, in place over dR:
