@@ -1,7 +1,8 @@
 // Backward pass of the tiled MonarchAttention forward (the
 // paper's finetuning backward, PAPER.md:135-136, 644 -- not in the reference
-// package, whose SPEC.md:8 leaves it out).  fp32 SIMT kernels over the factors
-// the forward exports (R' and L' of every refinement, factors.py:57-79 layout),
+// package, whose SPEC.md:8 leaves it out).  Batched contractions (TF32 mma.sync for
+// bf16 I/O, fp32 SIMT for fp32 I/O) and row kernels over the fp32 factors the
+// forward exports (R' and L' of every refinement, factors.py:57-79 layout),
 // restating the chain rule of solver.py:184-195 / factors.py:123-124:
 //
 //   forward per refinement t:  z = A_t K^T,  R = softmax_i z,  aL = R K,
