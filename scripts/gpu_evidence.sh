@@ -6,6 +6,7 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/ev/pytest_gpu.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ev/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/ev/smoke.log
 timeout 900 python bench.py > gpurun_out/ev/bench_default.json 2> gpurun_out/ev/bench_default.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/ev/bench_reference.json 2> gpurun_out/ev/bench_reference.err
+timeout 300 python scripts/bwd_profile.py > gpurun_out/ev/bwd_profile.txt 2>&1
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
     bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > gpurun_out/ev/bench_torchrun1.json 2> gpurun_out/ev/bench_torchrun1.err
 # two ranks sharing the box's one GPU (self-launched under torch.distributed.run; gloo barrier / max)
