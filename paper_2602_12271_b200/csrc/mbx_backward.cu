@@ -26,6 +26,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <mutex>
+#include <type_traits>
 
 namespace mbx {
 namespace {
@@ -617,58 +618,56 @@ __device__ __forceinline__ int64_t slot_row(const Geometry& g, const int32_t* or
     return order ? (int64_t)order[p] : p;
 }
 
-// dst[bh][tile][r][j][e] = scale * src[b, h, row(tile, r, j), e]: one warp per slot row
-// (the row's token index and source offset computed once, lanes over e)
-template <typename T>
-__global__ void gather_tiles(const Geometry g, const T* __restrict__ src, const int64_t* st, const int32_t* order,
-                             int tiles, int width, float scale, float* __restrict__ dst) {
-    const int64_t rows = (int64_t)g.bh * tiles * g.s1 * g.s2;
-    const int lane = threadIdx.x & 31;
-    const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        uint32_t x = (uint32_t)w;   // rows < 2^32 (host-checked)
-        const int j = (int)(x % (uint32_t)g.s2); x /= (uint32_t)g.s2;
-        const int r = (int)(x % (uint32_t)g.s1); x /= (uint32_t)g.s1;
-        const int tile = (int)(x % (uint32_t)tiles);
-        const int bh = (int)(x / (uint32_t)tiles);
-        const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
-        const T* sp = src + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
-        float* dp = dst + w * width;
-        if (width % 128 == 0 && ((uintptr_t)sp % (4 * sizeof(T))) == 0) {   // 4 elements per lane
-            for (int e = 4 * lane; e < width; e += 128) {
-                float4 x = ld4(sp + e);
-                store4(dp + e, make_float4(scale * x.x, scale * x.y, scale * x.z, scale * x.w));
-            }
-        } else {
-            for (int e = lane; e < width; e += 32) dp[e] = scale * ld(sp + e);
-        }
-    }
+// token-order offset of slot row w (bh, tile, r, j) in a (B, H, N, width) tensor with strides st
+__device__ __forceinline__ int64_t slot_offset(const Geometry& g, const int32_t* order, int tiles, uint32_t w,
+                                               int64_t s0, int64_t s1, int64_t s2) {
+    const int j = (int)(w % (uint32_t)g.s2); w /= (uint32_t)g.s2;
+    const int r = (int)(w % (uint32_t)g.s1); w /= (uint32_t)g.s1;
+    const int tile = (int)(w % (uint32_t)tiles);
+    const int bh = (int)(w / (uint32_t)tiles);
+    const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
+    return b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
 }
 
-template <typename T>
-__global__ void scatter_tiles(const Geometry g, const float* __restrict__ src, const int64_t* st, const int32_t* order,
-                              int tiles, int width, float scale, T* __restrict__ dst) {
+// dst[bh][tile][r][j][e] = scale * src[b, h, row(tile, r, j), e] (gather) and back (scatter):
+// one warp per kRowsPerWarp slot rows, lanes over e.  With width 128 and 16-byte aligned rows
+// all of a warp's rows are loaded before any is stored (4 x 16 B in flight per lane: with one
+// row per warp the copy ran at ~2 TB/s, latency-bound); otherwise a scalar loop per row.
+constexpr int kRowsPerWarp = 4;
+template <typename T, bool GATHER>
+__global__ void copy_tiles(const Geometry g, const void* __restrict__ src_, const int64_t* st, const int32_t* order,
+                           int tiles, int width, float scale, void* __restrict__ dst_) {
+    using S = typename std::conditional<GATHER, T, float>::type;   // source element
+    using D = typename std::conditional<GATHER, float, T>::type;   // destination element
+    const S* src = static_cast<const S*>(src_);
+    D* dst = static_cast<D*>(dst_);
     const int64_t rows = (int64_t)g.bh * tiles * g.s1 * g.s2;
     const int lane = threadIdx.x & 31;
     const int64_t s0 = st[0], s1 = st[1], s2 = st[2];
-    for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < rows;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        uint32_t x = (uint32_t)w;   // rows < 2^32 (host-checked)
-        const int j = (int)(x % (uint32_t)g.s2); x /= (uint32_t)g.s2;
-        const int r = (int)(x % (uint32_t)g.s1); x /= (uint32_t)g.s1;
-        const int tile = (int)(x % (uint32_t)tiles);
-        const int bh = (int)(x / (uint32_t)tiles);
-        const int b = bh / g.heads, h = bh - (bh / g.heads) * g.heads;
-        T* dp = dst + b * s0 + h * s1 + slot_row(g, order, tile, r, j) * s2;
-        const float* sp = src + w * width;
-        if (width % 128 == 0 && ((uintptr_t)dp % (4 * sizeof(T))) == 0) {
-            for (int e = 4 * lane; e < width; e += 128) {
-                float4 x = ld4(sp + e);
-                store4(dp + e, make_float4(scale * x.x, scale * x.y, scale * x.z, scale * x.w));
-            }
+    const bool vec = width == 128 && (s0 % 4) == 0 && (s1 % 4) == 0 && (s2 % 4) == 0 &&
+                     ((uintptr_t)(GATHER ? (const void*)src : (const void*)dst) % (4 * sizeof(T))) == 0;
+    for (int64_t w0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * kRowsPerWarp; w0 < rows;
+         w0 += (((int64_t)gridDim.x * blockDim.x) >> 5) * kRowsPerWarp) {
+        int64_t tok[kRowsPerWarp];
+#pragma unroll
+        for (int u = 0; u < kRowsPerWarp; ++u)
+            tok[u] = w0 + u < rows ? slot_offset(g, order, tiles, (uint32_t)(w0 + u), s0, s1, s2) : 0;
+        if (vec) {
+            float4 x[kRowsPerWarp];
+#pragma unroll
+            for (int u = 0; u < kRowsPerWarp; ++u)
+                if (w0 + u < rows) x[u] = ld4(src + (GATHER ? tok[u] : (w0 + u) * width) + 4 * lane);
+#pragma unroll
+            for (int u = 0; u < kRowsPerWarp; ++u)
+                if (w0 + u < rows)
+                    store4(dst + (GATHER ? (w0 + u) * width : tok[u]) + 4 * lane,
+                           make_float4(scale * x[u].x, scale * x[u].y, scale * x[u].z, scale * x[u].w));
         } else {
-            for (int e = lane; e < width; e += 32) store(dp + e, scale * sp[e]);
+            for (int u = 0; u < kRowsPerWarp && w0 + u < rows; ++u) {
+                const S* sp = src + (GATHER ? tok[u] : (w0 + u) * width);
+                D* dp = dst + (GATHER ? (w0 + u) * width : tok[u]);
+                for (int e = lane; e < width; e += 32) store(dp + e, scale * ld(sp + e));
+            }
         }
     }
 }
@@ -926,15 +925,15 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
     // gathers / scatters: one warp per slot row, all rows resident in one pass
     const int64_t slot_rows = bh * (gq > gk ? gq : gk) * s1 * s2;
     if (slot_rows >= (int64_t)UINT32_MAX) return cudaErrorInvalidValue;
-    const unsigned gb = (unsigned)((slot_rows + 7) / 8);
+    const unsigned gb = (unsigned)((slot_rows + 8 * kRowsPerWarp - 1) / (8 * kRowsPerWarp));
     { ProfScope ps_("bwd_gather", stream);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt); }
+    copy_tiles<T, true><<<gb, 256, 0, stream>>>(g, q, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, b.Qt); }
     { ProfScope ps_("bwd_gather", stream);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, k, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, b.Kt); }
+    copy_tiles<T, true><<<gb, 256, 0, stream>>>(g, k, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, b.Kt); }
     { ProfScope ps_("bwd_gather", stream);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, v, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, b.Vt); }
+    copy_tiles<T, true><<<gb, 256, 0, stream>>>(g, v, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, b.Vt); }
     { ProfScope ps_("bwd_gather", stream);
-    gather_tiles<T><<<gb, 256, 0, stream>>>(g, dout, dstr + 9, g.q_order, (int)gq, (int)dv, 1.f, b.dOt); }
+    copy_tiles<T, true><<<gb, 256, 0, stream>>>(g, dout, dstr + 9, g.q_order, (int)gq, (int)dv, 1.f, b.dOt); }
     cudaMemsetAsync(b.dQt, 0, sizeof(float) * bh * tq * d, stream);
     cudaMemsetAsync(b.dKt, 0, sizeof(float) * bh * tk * d, stream);
     cudaMemsetAsync(b.dVt, 0, sizeof(float) * bh * tk * dv, stream);
@@ -1059,11 +1058,11 @@ cudaError_t backward_t(const Geometry& g, const T* q, const T* k, const T* v, co
     }
     // scatter back to token order: dq = scale * dQt (Q entered the solver as scale * q)
     { ProfScope ps_("bwd_scatter", stream);
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dQt, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, dq_out); }
+    copy_tiles<T, false><<<gb, 256, 0, stream>>>(g, b.dQt, dstr + 0, g.q_order, (int)gq, (int)d, g.scale, dq_out); }
     { ProfScope ps_("bwd_scatter", stream);
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dKt, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, dk_out); }
+    copy_tiles<T, false><<<gb, 256, 0, stream>>>(g, b.dKt, dstr + 3, g.kv_order, (int)gk, (int)d, 1.f, dk_out); }
     { ProfScope ps_("bwd_scatter", stream);
-    scatter_tiles<T><<<gb, 256, 0, stream>>>(g, b.dVt, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, dv_out); }
+    copy_tiles<T, false><<<gb, 256, 0, stream>>>(g, b.dVt, dstr + 6, g.kv_order, (int)gk, (int)dv, 1.f, dv_out); }
     (void)nb_ak;
     return cudaGetLastError();
 }
