@@ -251,6 +251,21 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const float* p) {
 template <int MODE>
 __device__ __forceinline__ void mma_issue_async(float* S, const float* P, int64_t s_row, int64_t s_k, int r0,
                                                 int rows, int k0, int K2, int tid) {
+    if (MODE < 2) {   // scalar modes: 4-byte cp.async per element, same element map as mma_load
+#pragma unroll
+        for (int r = 0; r < kMT * kMK / kMThreads; ++r) {
+            const int row = MODE == 1 ? tid / kMK + (kMThreads / kMK) * r : tid % kMT;
+            const int kk = MODE == 1 ? tid % kMK : tid / kMT + (kMThreads / kMT) * r;
+            const bool ok = r0 + row < rows && k0 + kk < K2;
+            const float* src = P + (int64_t)(r0 + row) * s_row + (int64_t)(k0 + kk) * s_k;
+            float* dst = MODE == 1 ? S + row * (kMK + 4) + kk : S + kk * (kMT + 8) + row;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(dst)),
+                         "l"(ok ? src : P), "r"(ok ? 4 : 0)
+                         : "memory");
+        }
+        return;
+    }
 #pragma unroll
     for (int r = 0; r < kMT * kMK / kMThreads / 4; ++r) {
         int row, kk;
@@ -273,6 +288,9 @@ __device__ __forceinline__ void mma_issue_async(float* S, const float* P, int64_
                      : "memory");
     }
 }
+#ifndef MBX_BWD_ASYNC_ALL
+#define MBX_BWD_ASYNC_ALL 1   // 0: registers-staged steps unless both operands are 16-byte aligned
+#endif
 #ifndef MBX_BWD_MINB
 #define MBX_BWD_MINB 6
 #endif
@@ -289,7 +307,7 @@ template <int AM, int BM>
 __global__ void __launch_bounds__(kMThreads, MBX_BWD_MINB) gemm_batched_tf32(Gemm G) {
     constexpr bool AK = AM & 1, BK = BM & 1;
     // both operands 16-byte aligned: a kMStages-deep cp.async ring, else registers-staged steps
-    constexpr bool ASYNC = AM >= 2 && BM >= 2;
+    constexpr bool ASYNC = MBX_BWD_ASYNC_ALL ? true : (AM >= 2 && BM >= 2);
     extern __shared__ __align__(16) float mma_smem[];
     const int tiles_n = (G.N + kMT - 1) / kMT;
     int64_t bx = blockIdx.x;
@@ -458,7 +476,7 @@ bool gemm_mma(Gemm G, cudaStream_t st) {
     const int am = mode(G.A, G.M), bm = mode(G.B, G.N);
 #define MBX_TF32_CASE(X, Y) \
     if (am == X && bm == Y) {                                                                          \
-        constexpr size_t smem = mma_smem_bytes(X >= 2 && Y >= 2);                                      \
+        constexpr size_t smem = mma_smem_bytes(MBX_BWD_ASYNC_ALL ? true : (X >= 2 && Y >= 2));                                      \
         if (smem > 48 * 1024 &&                                                                        \
             cudaFuncSetAttribute(gemm_batched_tf32<X, Y>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                  (int)smem) != cudaSuccess)                                            \
@@ -870,13 +888,12 @@ void gemm(Ctx& c, const char* name, int M, int N, int K1, int K2, const int nb[4
     const int64_t batches = (int64_t)nb[0] * nb[1] * nb[2] * nb[3];
     ProfScope p(name, c.st);
     // bf16 I/O: the in-library TF32 kernel, except for the contractions where cuBLAS's
-    // batched TF32 GEMM measured faster at C2 (scripts/bwd_profile.py, profiles/r2k_*):
-    // the two with row-contiguous operands on both sides (the kernel's scalar fragment
-    // reads) and the three s2 x s2 outputs reduced over d.  MBX_BWD_CUBLAS overrides the
-    // list ("all", "none", or comma-separated names; A/B only).
+    // batched GEMM measured faster at C2 (scripts/bwd_profile.py, profiles/r2v_*): the two
+    // with row-contiguous operands on both sides (the kernel's scalar fragment reads).
+    // MBX_BWD_CUBLAS overrides the list ("all", "none", or comma-separated names; A/B only).
     static const char* cublas_names = [] {
         const char* e = getenv("MBX_BWD_CUBLAS");
-        return e ? e : "bwd_dalpha_l,bwd_dy,bwd_dr_k,bwd_dr_v,bwd_z";
+        return e ? e : "bwd_dalpha_l,bwd_dy";
     }();
     if (c.tf32) {
         bool prefer_cublas = strcmp(cublas_names, "all") == 0;
